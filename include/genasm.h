@@ -1,0 +1,144 @@
+/*
+ * genasm.h -- C ABI of the B200-native improved-GenASM windowed aligner.
+ *
+ * The reference (`bitalign` 0.1.0, pure Python) has no FFI; its drop-in
+ * boundary for the hot path is the Python API
+ *     align(pattern, text, cfg)          pkg/src/bitalign/window.py:85-129
+ *     align_batch(pairs, cfg, parallel)  pkg/src/bitalign/window.py:152-163
+ *     WindowConfig                       pkg/src/bitalign/window.py:44-70
+ *     AlignmentResult / BatchOutcome     pkg/src/bitalign/window.py:73-82, 132-141
+ * The entry points below are what a binding of that API binds: one batched
+ * call with plain pointers and sizes (no torch types), per-pair failures
+ * returned as data (BatchOutcome.error), library errors as a return code +
+ * ga_last_error().  The Python package paper_2203_15561_b200 binds this via
+ * ctypes; INTEGRATION.md shows the stub a bitalign maintainer would add.
+ *
+ * Symbol codes (pkg/src/bitalign/distance.py:31, 70-79):
+ *     0=A 1=C 2=G 3=T, 4=any other code unit (never matches, not even itself,
+ *     lowercase included -- align() does not uppercase).
+ */
+#ifndef GENASM_H
+#define GENASM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GA_MAX_WINDOW 128   /* kernel-supported window (configs need <= 128) */
+
+/* Per-pair status (BatchOutcome.ok / .error; pkg/src/bitalign/window.py:144-149). */
+enum {
+    GA_OK = 0,
+    GA_WINDOW_FAILED = 1,   /* "WindowFailed: window {i} found no alignment within k={k}" */
+    GA_EMPTY_PATTERN = 2,   /* "EmptyPattern: pattern must not be empty" */
+    GA_STUCK = 3,           /* StuckTraceback / PrunedAccess tripwire (never on valid tables) */
+};
+
+/* Driver parameters: WindowConfig (pkg/src/bitalign/window.py:44-70).
+ * k must already be resolved (k=None -> window).  priority is a
+ * permutation of "MSID" (pkg/src/bitalign/backtrace.py:64-67). */
+typedef struct {
+    int32_t window;
+    int32_t overlap;
+    int32_t k;
+    char    priority[4];
+} ga_config;
+
+/* A batch of (pattern, text) pairs: the `pairs` list of align_batch.
+ * All sequences live in one code array; offsets index into it. */
+typedef struct {
+    int64_t        n_pairs;
+    const uint8_t* codes;      /* symbol codes 0..4 */
+    int64_t        codes_len;  /* bytes in `codes` (for host->device copies) */
+    const int64_t* pat_off;
+    const int32_t* pat_len;
+    const int64_t* txt_off;
+    const int32_t* txt_len;
+    const int32_t* order;      /* optional processing order (a permutation of
+                                  0..n_pairs-1, longest first for load balance);
+                                  NULL: ga_align_batch computes it on the host,
+                                  ga_align_batch_device uses input order */
+} ga_batch_in;
+
+/* One AlignmentResult (pkg/src/bitalign/window.py:73-82) or its failure.
+ * 64 bytes, one D2H copy per batch. */
+typedef struct {
+    int32_t status;           /* GA_OK / GA_WINDOW_FAILED / GA_EMPTY_PATTERN / GA_STUCK */
+    int32_t fail_window;      /* WindowFailed.window_index, else -1 */
+    int64_t cost;             /* AlignmentResult.cost */
+    int64_t text_consumed;    /* AlignmentResult.text_consumed */
+    int64_t rows_computed;    /* AlignmentResult.rows_computed */
+    int64_t ops_len;          /* len(AlignmentResult.cigar) */
+    int64_t entry_reads;      /* AccessCounters.entry_reads   (dptable.py:85-105) */
+    int64_t entry_writes;     /* AccessCounters.entry_writes */
+    int64_t words_allocated;  /* AccessCounters.words_allocated */
+} ga_pair_result;
+
+/* Caller-allocated outputs.  ops_off/win_off are caller-computed prefix
+ * sums: capacity pat_len+txt_len ops per pair and ga_num_windows() window
+ * distances per pair. */
+typedef struct {
+    ga_pair_result* results;          /* n_pairs */
+    const int64_t*  ops_off;          /* n_pairs */
+    uint8_t*        ops;              /* ASCII '=','X','I','D' in walk (= forward) order */
+    int64_t         ops_capacity;     /* bytes in `ops` */
+    const int64_t*  win_off;          /* n_pairs */
+    uint8_t*        window_distances; /* AlignmentResult.window_distances, d_min per window */
+    int64_t         win_capacity;     /* entries in `window_distances` */
+} ga_batch_out;
+
+typedef struct ga_ctx ga_ctx;
+
+/* Library version string. */
+const char* ga_version(void);
+
+/* Number of windows align() walks for a pattern of length `pattern_len`
+ * (1 + ceil(max(0, |P|-W)/(W-O)); 0 for an empty pattern). */
+int64_t ga_num_windows(int64_t pattern_len, int32_t window, int32_t overlap);
+
+/* Validate a config exactly as WindowConfig.__post_init__ plus the kernel's
+ * window limit.  Returns 0 or writes a message into msg (may be NULL). */
+int ga_check_config(const ga_config* cfg, char* msg, int msg_len);
+
+/* Encode code units to symbol codes: 'A','C','G','T' -> 0..3, anything
+ * else -> 4 (pkg/src/bitalign/distance.py:70-79: only the exact
+ * uppercase alphabet has masks). */
+void ga_encode_ascii(const char* seq, int64_t n, uint8_t* out);
+
+/* Create a context bound to one CUDA device (one context per device; a
+ * context is not re-entrant).  Returns 0 or a CUDA error code. */
+int ga_create(int device, ga_ctx** out);
+void ga_destroy(ga_ctx* ctx);
+const char* ga_last_error(const ga_ctx* ctx);
+
+/* align_batch (pkg/src/bitalign/window.py:152-163) over HOST buffers:
+ * host->device copies, the fused DC+TB kernel, device->host copies, all on
+ * the context's stream; returns when the results are in `out`.  Results are
+ * in input order and independent of batch composition. */
+int ga_align_batch(ga_ctx* ctx, const ga_batch_in* in, const ga_config* cfg,
+                   ga_batch_out* out);
+
+/* Same call over DEVICE-resident buffers (every pointer in `in` and `out`
+ * is a device pointer on the context's device).  Asynchronous on
+ * `stream` (a cudaStream_t; NULL = the context's own stream). */
+int ga_align_batch_device(ga_ctx* ctx, const ga_batch_in* in, const ga_config* cfg,
+                          ga_batch_out* out, void* stream);
+
+/* Kernel launches issued by the last ga_align_batch* call (bench evidence). */
+int64_t ga_last_launch_count(const ga_ctx* ctx);
+
+/* Longest-first processing order (LPT) by pattern length: the host-side
+ * length bucketing that balances mixed read lengths. */
+void ga_lpt_order(int64_t n_pairs, const int32_t* pat_len, int32_t* order_out);
+
+/* Pinned host memory for zero-staging host<->device copies (bench e2e). */
+void* ga_host_alloc(int64_t bytes);
+void ga_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GENASM_H */

@@ -1,0 +1,182 @@
+"""Device engine: loads the in-tree sm_100a library and runs packed batches.
+
+There is no CPU fallback.  If ``_genasm.so`` is missing or no CUDA device is
+visible, every call raises -- the product path never routes around the
+kernel.  One ``ga_ctx`` (stream + device buffers) is kept per device; a
+multi-device batch is split longest-first across devices and each device is
+driven from its own host thread (ctypes releases the GIL during the call).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from ._abi import PackedBatch, PackedResults
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "_genasm.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+_ctxs: dict[int, C.c_void_p] = {}
+_ctx_locks: dict[int, threading.Lock] = {}
+
+
+class ExtensionMissing(RuntimeError):
+    """The CUDA extension is not built; there is deliberately no fallback."""
+
+
+def lib():
+    """Load _genasm.so (declaring every C-ABI signature); raise if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(SO_PATH):
+            raise ExtensionMissing(
+                f"{SO_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (the GPU path has no CPU fallback)")
+        L = C.CDLL(SO_PATH)
+        B = C.POINTER(_abi.GaBatchIn)
+        O = C.POINTER(_abi.GaBatchOut)
+        F = C.POINTER(_abi.GaConfig)
+        sigs = {
+            "ga_version": ([], C.c_char_p),
+            "ga_num_windows": ([C.c_int64, C.c_int32, C.c_int32], C.c_int64),
+            "ga_check_config": ([F, C.c_char_p, C.c_int], C.c_int),
+            "ga_encode_ascii": ([C.c_char_p, C.c_int64, C.c_void_p], None),
+            "ga_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+            "ga_destroy": ([C.c_void_p], None),
+            "ga_last_error": ([C.c_void_p], C.c_char_p),
+            "ga_align_batch": ([C.c_void_p, B, F, O], C.c_int),
+            "ga_align_batch_device": ([C.c_void_p, B, F, O, C.c_void_p], C.c_int),
+            "ga_last_launch_count": ([C.c_void_p], C.c_int64),
+            "ga_lpt_order": ([C.c_int64, C.c_void_p, C.c_void_p], None),
+            "ga_host_alloc": ([C.c_int64], C.c_void_p),
+            "ga_host_free": ([C.c_void_p], None),
+        }
+        for name, (args, res) in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def context(device: int = 0) -> C.c_void_p:
+    """The per-device ga_ctx (created on first use)."""
+    L = lib()
+    with _lib_lock:
+        ctx = _ctxs.get(device)
+        if ctx is None:
+            ctx = C.c_void_p()
+            rc = L.ga_create(int(device), C.byref(ctx))
+            if rc != 0:
+                raise RuntimeError(
+                    f"ga_create(device={device}) failed with CUDA error {rc}: no usable CUDA "
+                    "device (the GPU path has no CPU fallback)")
+            _ctxs[device] = ctx
+            _ctx_locks[device] = threading.Lock()
+        return ctx
+
+
+def _default_device() -> int:
+    env = os.environ.get("LOCAL_RANK")
+    return int(env) if env is not None and env.isdigit() else 0
+
+
+def lpt_order(pat_len: np.ndarray) -> np.ndarray:
+    """Longest-first order (host length bucketing)."""
+    order = np.empty(pat_len.shape[0], dtype=np.int32)
+    lib().ga_lpt_order(int(pat_len.shape[0]), np.ascontiguousarray(pat_len, np.int32).ctypes.data,
+                       order.ctypes.data)
+    return order
+
+
+def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: str,
+               device: int | None = None) -> PackedResults:
+    """One ga_align_batch call on one device (host buffers in and out)."""
+    dev = _default_device() if device is None else int(device)
+    ctx = context(dev)
+    out = PackedResults.allocate(batch, window, overlap)
+    if batch.n_pairs == 0:
+        return out
+    cfg = _abi.make_config(window, overlap, k, priority)
+    bin_ = batch.struct()
+    bout = out.struct()
+    with _ctx_locks[dev]:
+        rc = lib().ga_align_batch(ctx, C.byref(bin_), C.byref(cfg), C.byref(bout))
+        if rc != 0:
+            raise RuntimeError(f"ga_align_batch failed ({rc}): "
+                               f"{lib().ga_last_error(ctx).decode(errors='replace')}")
+    return out
+
+
+def split_lpt(pat_len: np.ndarray, window: int, overlap: int, n_shards: int) -> list[np.ndarray]:
+    """Greedy LPT partition of pair indices by window count (the exact cost
+    proxy: #windows follows from |P| alone)."""
+    cost = _abi.num_windows(pat_len, window, overlap).astype(np.int64)
+    order = np.argsort(-cost, kind="stable")
+    loads = np.zeros(n_shards, dtype=np.int64)
+    owner = np.empty(pat_len.shape[0], dtype=np.int64)
+    for idx in order:
+        s = int(np.argmin(loads))
+        owner[idx] = s
+        loads[s] += max(1, int(cost[idx]))
+    return [np.nonzero(owner == s)[0] for s in range(n_shards)]
+
+
+def _subset(batch: PackedBatch, idx: np.ndarray) -> PackedBatch:
+    return PackedBatch(codes=batch.codes, pat_off=batch.pat_off[idx], pat_len=batch.pat_len[idx],
+                       txt_off=batch.txt_off[idx], txt_len=batch.txt_len[idx])
+
+
+def _scatter(full: PackedResults, part: PackedResults, idx: np.ndarray, batch: PackedBatch) -> None:
+    full.results[idx] = part.results
+    for local, q in enumerate(idx.tolist()):
+        n_ops = int(part.results["ops_len"][local])
+        src = int(part.ops_off[local])
+        dst = int(full.ops_off[q])
+        full.ops[dst:dst + n_ops] = part.ops[src:src + n_ops]
+        w_src = int(part.win_off[local])
+        w_dst = int(full.win_off[q])
+        w_n = (int(part.win_off[local + 1]) if local + 1 < len(idx) else part.dists.shape[0]) - w_src
+        full.dists[w_dst:w_dst + w_n] = part.dists[w_src:w_src + w_n]
+
+
+def run_batch(batch: PackedBatch, cfg, devices=None) -> PackedResults:
+    """align_batch on one or more devices; results always in input order."""
+    if devices is None or (isinstance(devices, int) and devices <= 1):
+        dev = None if devices is None else 0
+        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev)
+    dev_list = list(range(devices)) if isinstance(devices, int) else [int(d) for d in devices]
+    if len(dev_list) == 1:
+        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev_list[0])
+    shards = split_lpt(batch.pat_len, cfg.window, cfg.overlap, len(dev_list))
+    parts: list[PackedResults | None] = [None] * len(dev_list)
+    errors: list[BaseException] = []
+
+    def work(s: int) -> None:
+        try:
+            parts[s] = run_packed(_subset(batch, shards[s]), cfg.window, cfg.overlap, cfg.k,
+                                  cfg.priority, dev_list[s])
+        except BaseException as exc:  # re-raised on the caller's thread
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(s,)) for s in range(len(dev_list))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    full = PackedResults.allocate(batch, cfg.window, cfg.overlap)
+    for s, idx in enumerate(shards):
+        if len(idx):
+            _scatter(full, parts[s], idx, batch)
+    return full

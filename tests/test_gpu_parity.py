@@ -1,0 +1,172 @@
+"""GPU parity: the sm_100a kernel (through the C-ABI) vs the reference's outputs.
+
+Three anchors, strongest first:
+  * golden fixtures produced by the reference itself (tests/golden/, made by
+    make_golden.py): known-answer vectors, a randomized corpus, and per-pair
+    digests of the BASELINE configs' recipe pairs;
+  * the C oracle (oracle/, pinned to the same fixtures by test_oracle.py) on
+    larger sets the reference is too slow to pre-compute, up to the full
+    138,929-pair config 3;
+  * size-independent properties at full size (replay validity, cost and span
+    consistency, batch-composition invariance).
+Equality is exact on every field: cigar, cost, text_consumed,
+window_distances, rows_computed, the three access counters, error strings.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import corpus
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import paper_2203_15561_b200 as ga
+    from paper_2203_15561_b200 import engine
+    engine.context(0)  # raises (no fallback) if the extension or device is missing
+    return ga
+
+
+def _cfg(ga, w, o, k, prio="MSID"):
+    return ga.WindowConfig(window=w, overlap=o, k=k, priority=prio)
+
+
+def _gpu_outcomes(ga, batch, cfg):
+    from paper_2203_15561_b200.engine import run_batch
+    from paper_2203_15561_b200.window import outcomes_from_packed
+    return outcomes_from_packed(batch, run_batch(batch, cfg), cfg)
+
+
+def test_extension_is_native(gpu):
+    from paper_2203_15561_b200 import engine
+    assert engine.lib().ga_version().decode().startswith("genasm-b200")
+
+
+def test_known_vectors(gpu):
+    with open(os.path.join(GOLD, "known.json")) as f:
+        known = json.load(f)
+    for case in known:
+        cfg = _cfg(gpu, case["window"], case["overlap"], case["k"], case["priority"])
+        got = gpu.align_batch([(case["pattern"], case["text"])], cfg)[0]
+        assert corpus.outcome_key(got) == case["key"], case
+
+
+def test_align_errors_and_types(gpu):
+    with pytest.raises(gpu.EmptyPattern):
+        gpu.align("", "ACGT")
+    with pytest.raises(gpu.WindowFailed) as info:
+        gpu.align("AAAAAAAA", "TTTTTTTT", gpu.WindowConfig(window=8, overlap=2, k=2))
+    assert info.value.window_index == 0 and info.value.k == 2
+    r = gpu.align("ACGTACGT", "ACGTACGT", gpu.WindowConfig(window=4, overlap=2, k=4))
+    assert r.cigar == "========" and r.window_distances == (0, 0, 0)
+    with pytest.raises(AttributeError):
+        r.cost = 7
+    assert gpu.align_batch([], gpu.WindowConfig()) == []
+    with pytest.raises(ValueError):
+        gpu.align("ACGT", "ACGT", gpu.WindowConfig(mode="baseline"))
+
+
+def test_fuzz_vs_reference_golden(gpu):
+    with open(os.path.join(GOLD, "fuzz.json")) as f:
+        gold = json.load(f)
+    for (case, ((w, o, k, prio), pairs)) in zip(gold["cases"],
+                                               corpus.fuzz_cases(gold["seed"], gold["batches"])):
+        assert case["cfg"] == [w, o, k, prio]
+        outs = gpu.align_batch(pairs, _cfg(gpu, w, o, k, prio))
+        got = [str(corpus.digest(x)) for x in outs]
+        bad = [q for q, (a, b) in enumerate(zip(got, case["digests"])) if a != b]
+        assert not bad, (case["cfg"], [pairs[q] for q in bad[:2]])
+
+
+def test_fuzz_vs_oracle(gpu, oracle_mod):
+    for (w, o, k, prio), pairs in corpus.fuzz_cases(777, 150, pairs_per_batch=16, max_len=700):
+        cfg = _cfg(gpu, w, o, k, prio)
+        got = [corpus.outcome_key(x) for x in gpu.align_batch(pairs, cfg)]
+        exp = [corpus.outcome_key(x) for x in oracle_mod.align_batch(pairs, cfg, threads=4)]
+        bad = [q for q in range(len(pairs)) if got[q] != exp[q]]
+        assert not bad, ((w, o, k, prio), pairs[bad[0]], got[bad[0]], exp[bad[0]])
+
+
+def _config_digest_check(gpu, cfg_id, key, w=64, o=24, k=64, count=None):
+    from paper_2203_15561_b200 import sim
+    gold = np.load(os.path.join(GOLD, "configs.npz"))[key]
+    n = len(gold) if count is None else count
+    batch, _ = sim.config_pairs(cfg_id, count=n)
+    outs = _gpu_outcomes(gpu, batch, _cfg(gpu, w, o, k))
+    got = np.array([corpus.digest(x) for x in outs], dtype=np.uint64)
+    bad = np.nonzero(got != gold[:n])[0]
+    assert bad.size == 0, f"{key}: {bad.size} mismatching pairs, first {bad[:5].tolist()}"
+
+
+def test_config1_all_pairs_vs_reference(gpu):
+    _config_digest_check(gpu, 1, "cfg1")
+
+
+def test_config2_all_pairs_vs_reference(gpu):
+    _config_digest_check(gpu, 2, "cfg2")
+
+
+def test_config3_prefix_vs_reference(gpu):
+    _config_digest_check(gpu, 3, "cfg3")
+
+
+def test_config4_prefix_vs_reference(gpu):
+    _config_digest_check(gpu, 4, "cfg4")
+
+
+@pytest.mark.parametrize("w,o,k", [(w, 3 * w // 8, k) for w in (32, 64, 128)
+                                   for k in (w // 4, w // 2, w)])
+def test_config5_sweep_vs_reference(gpu, w, o, k):
+    _config_digest_check(gpu, 5, f"cfg5_w{w}_k{k}", w=w, o=o, k=k)
+
+
+def _packed_equal(a, b, tag=""):
+    if not np.array_equal(a.results, b.results):
+        bad = np.nonzero(a.results != b.results)[0]
+        raise AssertionError(f"{tag}: {bad.size} result records differ; first {bad[:4].tolist()}: "
+                             f"gpu={a.results[bad[0]]} oracle={b.results[bad[0]]}")
+    for q in range(a.results.shape[0]):
+        n = int(a.results["ops_len"][q])
+        oa, ob = int(a.ops_off[q]), int(b.ops_off[q])
+        assert np.array_equal(a.ops[oa:oa + n], b.ops[ob:ob + n]), q
+    assert np.array_equal(a.dists, b.dists)
+
+
+def test_config3_vs_oracle_4096(gpu, oracle_mod):
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(3, count=4096)
+    got = run_packed(batch, 64, 24, 64, "MSID")
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    _packed_equal(got, exp)
+
+
+def test_config5_vs_oracle_all_pairs(gpu, oracle_mod):
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(5)
+    for (w, o, k) in [(64, 24, 16), (128, 48, 128), (32, 12, 8)]:
+        got = run_packed(batch, w, o, k, "MSID")
+        exp = oracle_mod.align_packed(batch, w, o, k, "MSID", threads=os.cpu_count())
+        _packed_equal(got, exp, (w, o, k))
+
+
+def test_batch_composition_invariance(gpu):
+    """Results of a pair do not depend on its batch (sharding correctness)."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed, split_lpt, _subset
+    batch, _ = sim.config_pairs(5, count=600)
+    full = run_packed(batch, 64, 24, 64, "MSID")
+    for idx in split_lpt(batch.pat_len, 64, 24, 3):
+        part = run_packed(_subset(batch, idx), 64, 24, 64, "MSID")
+        assert np.array_equal(part.results, full.results[idx])
