@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/genasm_sim.h"
+
 namespace {
 
 struct MT {

@@ -1,0 +1,148 @@
+"""Host-side API (CPU only): the drop-in names, validation, packing and the
+C-ABI library's exports.  No compute call needs a GPU here."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2203_15561_b200 as ga
+from paper_2203_15561_b200 import _abi, engine
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_names_exported():
+    for name in ("align", "align_batch", "WindowConfig", "AlignmentResult", "BatchOutcome",
+                 "WindowFailed", "EmptyPattern", "AccessCounters"):
+        assert hasattr(ga, name)
+
+
+def test_config_defaults_and_validation():
+    cfg = ga.WindowConfig()
+    assert (cfg.window, cfg.overlap, cfg.k, cfg.mode, cfg.priority) == (64, 24, 64, "improved",
+                                                                         "MSID")
+    assert ga.WindowConfig(window=32).k == 32
+    for kwargs in (dict(window=8, overlap=8), dict(window=8, overlap=-1), dict(window=8, k=9),
+                   dict(window=8, k=0), dict(mode="turbo"), dict(priority="MMSS"),
+                   dict(window=0)):
+        with pytest.raises(ValueError):
+            ga.WindowConfig(**kwargs)
+
+
+@pytest.mark.reference
+def test_validation_messages_match_reference(reference):
+    from bitalign.window import WindowConfig as RefConfig
+    for kwargs in (dict(window=8, overlap=8), dict(window=8, overlap=-1), dict(window=8, k=9),
+                   dict(window=8, k=0), dict(mode="turbo"), dict(priority="MMSS"),
+                   dict(window=0)):
+        with pytest.raises(ValueError) as a:
+            RefConfig(**kwargs)
+        with pytest.raises(ValueError) as b:
+            ga.WindowConfig(**kwargs)
+        assert str(a.value) == str(b.value)
+
+
+def test_errors_before_any_device_work():
+    with pytest.raises(ga.EmptyPattern, match="pattern must not be empty"):
+        ga.align("", "ACGT")
+    with pytest.raises(ValueError, match="no GPU path"):
+        ga.align("ACGT", "ACGT", ga.WindowConfig(mode="baseline"))
+    with pytest.raises(ValueError, match="kernel maximum"):
+        ga.align_batch([("ACGT", "ACGT")], ga.WindowConfig(window=129))
+    e = ga.WindowFailed(3, 16)
+    assert str(e) == "window 3 found no alignment within k=16"
+    assert (e.window_index, e.k) == (3, 16)
+
+
+def test_encode_symbols():
+    assert _abi.encode("ACGTacgtNX").tolist() == [0, 1, 2, 3, 4, 4, 4, 4, 4, 4]
+    assert _abi.encode("AÇG").tolist() == [0, 4, 2]
+
+
+def test_packing_roundtrip():
+    pairs = [("ACGT", "AC"), ("", "T"), ("GG", ""), ("AÇG", "ng")]
+    b = _abi.PackedBatch.from_pairs(pairs)
+    assert b.n_pairs == 4
+    assert b.pat_len.tolist() == [4, 0, 2, 3] and b.txt_len.tolist() == [2, 1, 0, 2]
+    for q, (p, t) in enumerate(pairs):
+        assert b.codes[b.pat_off[q]:b.pat_off[q] + len(p)].tolist() == _abi.encode(p).tolist()
+        assert b.codes[b.txt_off[q]:b.txt_off[q] + len(t)].tolist() == _abi.encode(t).tolist()
+
+
+def test_num_windows_formula():
+    # 4 windows for 150 bp, 6 for 250 bp, 250 for 10 kb
+    assert [_abi.num_windows(x, 64, 24) for x in (0, 1, 64, 65, 150, 250, 10_000)] == \
+        [0, 1, 1, 2, 4, 6, 250]
+
+
+def test_outcomes_from_packed_shapes():
+    b = _abi.PackedBatch.from_pairs([("ACGT", "ACGT"), ("AAAA", "TTTT"), ("", "A")])
+    out = _abi.PackedResults.allocate(b, 64, 24)
+    out.results[0] = (0, -1, 0, 4, 1, 4, 3, 4, 4)
+    out.ops[out.ops_off[0]:out.ops_off[0] + 4] = np.frombuffer(b"====", np.uint8)
+    out.dists[out.win_off[0]] = 0
+    out.results[1] = (1, 0, 0, 0, 0, 0, 0, 0, 0)
+    out.results[2] = (2, -1, 0, 0, 0, 0, 0, 0, 0)
+    outs = ga.window.outcomes_from_packed(b, out, ga.WindowConfig(window=64, k=2))
+    assert outs[0].ok and outs[0].result.cigar == "====" and outs[0].result.window_distances == (0,)
+    assert outs[1].error == "WindowFailed: window 0 found no alignment within k=2"
+    assert outs[2].error == "EmptyPattern: pattern must not be empty"
+
+
+def test_lpt_split_balances_and_partitions():
+    rng = np.random.default_rng(0)
+    lens = rng.integers(100, 50_000, size=1000).astype(np.int32)
+    shards = engine.split_lpt(lens, 64, 24, 8)
+    allidx = np.sort(np.concatenate(shards))
+    assert np.array_equal(allidx, np.arange(1000))
+    loads = [int(_abi.num_windows(lens[s], 64, 24).sum()) for s in shards]
+    assert max(loads) - min(loads) <= int(_abi.num_windows(lens, 64, 24).max())
+
+
+# ---------------------------------------------------------------------------
+# C-ABI library: loads without a GPU and exports every symbol include/genasm.h declares
+
+
+def _header_functions():
+    text = "".join(open(os.path.join(ROOT, "include", h)).read()
+                   for h in ("genasm.h", "genasm_sim.h"))
+    return sorted(set(re.findall(r"\b(ga_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_capi_exports_every_declared_symbol():
+    L = engine.lib()
+    names = _header_functions()
+    assert len(names) >= 19
+    for name in names:
+        assert hasattr(L, name), name
+
+
+def test_capi_host_functions():
+    L = engine.lib()
+    assert L.ga_version().decode().startswith("genasm-b200")
+    for n, w, o in ((0, 64, 24), (150, 64, 24), (10_000, 64, 24), (333, 32, 12), (64, 64, 0)):
+        assert L.ga_num_windows(n, w, o) == _abi.num_windows(n, w, o)
+    msg = C.create_string_buffer(160)
+    assert L.ga_check_config(C.byref(_abi.make_config(64, 24, 64, "MSID")), msg, 160) == 0
+    assert L.ga_check_config(C.byref(_abi.make_config(8, 8, 8, "MSID")), msg, 160) == 1
+    assert msg.value.decode() == "overlap must be in [0, window), got 8 for window 8"
+    assert L.ga_check_config(C.byref(_abi.make_config(8, 2, 9, "MSID")), msg, 160) == 1
+    assert msg.value.decode() == "k must be in [1, 8], got 9"
+    assert L.ga_check_config(C.byref(_abi.make_config(256, 2, 9, "MSID")), msg, 160) == 1
+    out = np.zeros(6, np.uint8)
+    L.ga_encode_ascii(b"ACGTNa", 6, out.ctypes.data)
+    assert out.tolist() == [0, 1, 2, 3, 4, 4]
+    lens = np.array([5, 9, 1, 9], np.int32)
+    assert engine.lpt_order(lens).tolist() == [1, 3, 0, 2]
+
+
+def test_no_cpu_fallback_when_extension_missing(monkeypatch, tmp_path):
+    monkeypatch.setattr(engine, "SO_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(engine, "_lib", None)
+    with pytest.raises(engine.ExtensionMissing):
+        engine.lib()
