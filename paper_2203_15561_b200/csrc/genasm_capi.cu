@@ -216,9 +216,8 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     e = cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     const int group = env_int("GA_GROUP", 8);
-    const int s_lv = env_int("GA_SLV", 8);
-    const int smem_budget = env_int("GA_SMEM_KB", 72) * 1024;
-    e = genasm::launch_genasm(P, group, s_lv, smem_budget, c->num_sms, st, &c->overflow, &c->overflow_cap,
+    const int block = env_int("GA_BLOCK", 64);
+    e = genasm::launch_genasm(P, group, block, c->num_sms, st, &c->overflow, &c->overflow_cap,
                               &c->last_shape);
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     c->launches = 1;

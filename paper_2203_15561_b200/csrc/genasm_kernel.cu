@@ -1,17 +1,21 @@
 // genasm_kernel.cu -- fused windowed GenASM-DC + GenASM-TB kernel (sm_100a).
-// See genasm_kernel.cuh for the design summary and DESIGN.md for the roofline.
+// Design summary in genasm_kernel.cuh; roofline and layout in DESIGN.md.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "genasm_kernel.cuh"
 
 namespace genasm {
 
-constexpr int kBlockThreads = 128;
+constexpr int kMaxBlock = 256;
 
-// ---- bit-row helpers (rows are NW little-endian 32-bit words, 0 = active) ----
+enum : int { NEED_PAIR = 0, NEED_WINDOW = 1, IN_DC = 2, IN_TB = 3, DONE = 4 };
+enum : int { OP_M = 0, OP_S = 1, OP_I = 2, OP_D = 3, OP_STOP = 4, OP_STUCK = 5 };
 
-// init(m, d): bits < min(d, m) are 0 (bitvec.py:108-122).  Bits >= m are
+// ---- bit rows: NW little-endian 32-bit words, 0 = active ----
+
+// init(m, d): bits < min(d, m) are 0 (bitvec.py:108-122); bits >= m are
 // don't-care and left 1.
 template <int NW>
 __device__ __forceinline__ void init_row(uint32_t (&r)[NW], int m, int d) {
@@ -43,80 +47,142 @@ __device__ __forceinline__ uint32_t word_sel(const uint32_t (&x)[NW], int w) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t bit_of(const uint32_t* e, int x) {
-    return (e[x >> 5] >> (x & 31)) & 1u;
+// 32-bit band of a row starting at bit `amt` (0 <= amt <= 32*NW-32)
+template <int NW>
+__device__ __forceinline__ uint32_t band32(const uint32_t (&r)[NW], int amt) {
+    if (NW == 1) return r[0];
+    if (NW == 2) return __funnelshift_rc(r[0], r[NW - 1], (unsigned)amt);
+    const int wi = amt >> 5;
+    const int wj = wi + 1 < NW ? wi + 1 : NW - 1;
+    return __funnelshift_r(word_sel<NW>(r, wi), word_sel<NW>(r, wj), (unsigned)(amt & 31));
 }
 
+template <int NW>
+struct Geo {
+    static constexpr int WMAX = 32 * NW;
+    static constexpr bool BAND = NW >= 2;     // 32-bit band entries (else full 32-bit rows)
+    static constexpr int LV = BAND ? 16 : 40;  // table levels resident in shared memory
+    static constexpr int TAB_W = LV * WMAX;    // words
+    static constexpr int GROUP_W = TAB_W + 2 * WMAX * NW + WMAX / 2;
+    static constexpr int BAND_MAX = 32 * NW - 32;
+};
+
 template <int NW, int G>
-__global__ void __launch_bounds__(kBlockThreads)
-genasm_window_kernel(const KernelParams P) {
+__global__ void __launch_bounds__(kMaxBlock)
+genasm_kernel(const KernelParams P) {
+    using GE = Geo<NW>;
+    constexpr int WMAX = GE::WMAX;
+    constexpr bool BAND = GE::BAND;
+    constexpr int LV = GE::LV;
     extern __shared__ uint32_t smem[];
-    constexpr int WMAX = 32 * NW;
     const int lane = threadIdx.x & 31;
     const int q = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     const unsigned lowmask = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
-    const int groups_per_block = kBlockThreads / G;
-    const int group_in_block = threadIdx.x / G;
-    const int W = P.W, O = P.O, K = P.k, S = P.s_lv;
+    const int gib = threadIdx.x / G;
+    const int groups_per_block = blockDim.x / G;
 
-    const int tab_words = S * W * NW;
-    const int group_words = tab_words + WMAX * NW + WMAX / 2;
-    uint32_t* tab = smem + group_in_block * group_words;
-    uint32_t* pmcol = tab + tab_words;
+    uint32_t* tab = smem + gib * GE::GROUP_W;
+    uint32_t* carry = tab + GE::TAB_W;
+    uint32_t* pmcol = carry + WMAX * NW;
     uint8_t* cp = reinterpret_cast<uint8_t*>(pmcol + WMAX * NW);
     uint8_t* ct = cp + WMAX;
-    const int64_t gid = (int64_t)blockIdx.x * groups_per_block + group_in_block;
+    const int64_t gid = (int64_t)blockIdx.x * groups_per_block + gib;
     uint32_t* gtab = P.overflow + gid * P.overflow_words_per_group;
-
-    auto entry = [&](int d, int j) -> uint32_t* {  // j in 1..n
-        return d < S ? tab + (d * W + (j - 1)) * NW : gtab + ((d - S) * W + (j - 1)) * NW;
-    };
-
+    const int W = P.W, O = P.O, K = P.k;
     PairResult* results = reinterpret_cast<PairResult*>(P.results);
 
-    for (;;) {
-        unsigned long long idx = 0;
-        if (q == 0) idx = atomicAdd(P.queue, 1ull);
-        idx = __shfl_sync(gmask, idx, 0, G);
-        if (idx >= (unsigned long long)P.n_pairs) break;
-        const int64_t pair = P.order ? (int64_t)P.order[idx] : (int64_t)idx;
-        const int32_t Lp = P.pat_len[pair];
-        const int32_t Lt = P.txt_len[pair];
-        const uint8_t* Pp = P.codes + P.pat_off[pair];
-        const uint8_t* Tp = P.codes + P.txt_off[pair];
-        uint8_t* ops = P.ops + P.ops_off[pair];
-        uint8_t* dists = P.dists + P.win_off[pair];
+    // ---- group-uniform state ----
+    int phase = NEED_PAIR;
+    int64_t pair = 0;
+    int Lp = 0, Lt = 0;
+    const uint8_t* Pp = nullptr;
+    const uint8_t* Tp = nullptr;
+    uint8_t* ops = nullptr;
+    uint8_t* dists = nullptr;
+    int64_t p = 0, t = 0, nops = 0;
+    int widx = 0, m = 0, n = 0, budget = 0, pass = 0, d_min = -1;
+    bool full = false;
+    // per-pair accumulators (meaningful in lane q == 0)
+    int64_t cost = 0, rows = 0, reads = 0, writes = 0, words = 0;
 
-        PairResult res;
-        res.status = 0; res.fail_window = -1; res.cost = 0; res.text_consumed = 0;
-        res.rows_computed = 0; res.ops_len = 0; res.entry_reads = 0; res.entry_writes = 0;
-        res.words_allocated = 0;
-        if (Lp <= 0) {
-            res.status = 2;  // EmptyPattern (window.py:87-88)
-            if (q == 0) results[pair] = res;
-            continue;
+    auto write_result = [&](int status, int fail_window) {
+        if (q == 0) {
+            PairResult r{};
+            r.status = status;
+            r.fail_window = fail_window;
+            if (status == 0) {
+                r.cost = cost;
+                r.text_consumed = t;
+                r.rows_computed = rows;
+                r.ops_len = nops;
+                r.entry_reads = reads;
+                r.entry_writes = writes;
+                r.words_allocated = words;
+            }
+            results[pair] = r;
         }
+    };
 
-        int64_t p = 0, t = 0;
-        int widx = 0;
-        while (p < Lp) {
+    // bit x of table entry (e, col), col >= 1; sets oob if outside the stored band
+    auto tbit = [&](int e, int col, int x, bool& oob) -> uint32_t {
+        if (BAND && full) {
+            const uint32_t* row = gtab + ((int64_t)e * W + (col - 1)) * NW;
+            return (row[x >> 5] >> (x & 31)) & 1u;
+        }
+        const uint32_t word = tab[e * WMAX + (col - 1)];
+        if (!BAND) return (word >> x) & 1u;
+        int amt = m - 1 - n + col - 15;
+        amt = amt < 0 ? 0 : (amt > GE::BAND_MAX ? GE::BAND_MAX : amt);
+        const int rel = x - amt;
+        if (rel < 0 || rel > 31) {
+            oob = true;
+            return 1u;
+        }
+        return (word >> rel) & 1u;
+    };
+
+    for (;;) {
+        // ================= setup: next pair / next window =================
+        while (phase == NEED_PAIR || phase == NEED_WINDOW) {
+            if (phase == NEED_PAIR) {
+                unsigned long long idx = 0;
+                if (q == 0) idx = atomicAdd(P.queue, 1ull);
+                idx = __shfl_sync(gmask, idx, 0, G);
+                if (idx >= (unsigned long long)P.n_pairs) {
+                    phase = DONE;
+                    break;
+                }
+                pair = P.order ? (int64_t)P.order[idx] : (int64_t)idx;
+                Lp = P.pat_len[pair];
+                Lt = P.txt_len[pair];
+                Pp = P.codes + P.pat_off[pair];
+                Tp = P.codes + P.txt_off[pair];
+                ops = P.ops + P.ops_off[pair];
+                dists = P.dists + P.win_off[pair];
+                p = t = nops = 0;
+                widx = 0;
+                cost = rows = reads = writes = words = 0;
+                if (Lp <= 0) {  // EmptyPattern (window.py:87-88)
+                    write_result(2, -1);
+                    continue;
+                }
+                phase = NEED_WINDOW;
+            }
             // ---- window geometry (window.py:96-101) ----
             const int64_t remaining = Lp - p;
             const bool final_w = remaining <= W;
-            const int m = final_w ? (int)remaining : W;
+            m = final_w ? (int)remaining : W;
             const int64_t tleft = Lt - t;
-            const int n = tleft < W ? (int)(tleft > 0 ? tleft : 0) : W;
-            const int budget = final_w ? m : W - O;
-
-            // ---- stage reversed chunks (window.py:99-100) ----
+            n = tleft < W ? (int)(tleft > 0 ? tleft : 0) : W;
+            budget = final_w ? m : W - O;
+            // ---- reversed chunks (window.py:99-100) ----
             __syncwarp(gmask);
             for (int i = q; i < m; i += G) cp[i] = Pp[p + m - 1 - i];
             for (int j = q; j < n; j += G) ct[j] = Tp[t + n - 1 - j];
             __syncwarp(gmask);
-
-            // ---- pattern masks (distance.py:70-79) and per-column masks (:91-94) ----
+            // ---- pattern masks (distance.py:70-79), per-column masks (:91-94) ----
             uint32_t mt[4][NW];
 #pragma unroll
             for (int c = 0; c < 4; ++c)
@@ -147,172 +213,231 @@ genasm_window_kernel(const KernelParams P) {
                     pmcol[j * NW + w] = x;
                 }
             }
-            __syncwarp(gmask);
-
-            // ---- GenASM-DC: levels-as-lanes wavefront with early termination ----
-            int d_min = -1;
-            if (n == 0) {
-                d_min = m <= K ? m : -1;  // R[d][0] = init(m,d) solves iff d >= m
+            pass = 0;
+            full = false;
+            if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
+                if (m <= K) {
+                    d_min = m;
+                    phase = IN_TB;
+                } else {
+                    write_result(1, widx);
+                    phase = NEED_PAIR;
+                }
             } else {
-                const int topw = (m - 1) >> 5;
-                const uint32_t topb = 1u << ((m - 1) & 31);
-                for (int pass = 0; pass * G <= K; ++pass) {
-                    const int d = pass * G + q;
-                    const bool active = d <= K;
-                    uint32_t v[NW], a[NW], outv[NW];
-                    init_row<NW>(v, m, d);
-                    init_row<NW>(a, m, d - 1 < 0 ? 0 : d - 1);
+                phase = IN_DC;
+            }
+        }
+        if (__all_sync(0xffffffffu, phase == DONE)) break;
+        __syncwarp();
+
+        // ================= DC pass round (all groups in lock-step) =================
+        {
+            const bool in_dc = phase == IN_DC;
+            const int d = pass * G + q;
+            const bool active = in_dc && d <= K;
+            uint32_t v[NW], a[NW], outv[NW];
+            init_row<NW>(v, m, d);
+            init_row<NW>(a, m, d > 0 ? d - 1 : 0);
+            const uint32_t lvl0 = d == 0 ? 0xffffffffu : 0u;  // level 0 has only the M edge
+            if (d == 0) {
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) outv[w] = 0u;
-                    bool succ = false;
-                    const int steps = n + G - 1;
-                    for (int s = 0; s < steps; ++s) {
-                        const int j = s - q + 1;
-                        uint32_t b[NW];
+                for (int w = 0; w < NW; ++w) a[w] = 0xffffffffu;
+            }
 #pragma unroll
-                        for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(gmask, outv[w], 1, G);
-                        const bool inrange = active && j >= 1 && j <= n;
-                        if (inrange) {
-                            if (q == 0 && d >= 1) {
-                                const uint32_t* src = entry(d - 1, j);
+            for (int w = 0; w < NW; ++w) outv[w] = 0u;
+            const int topw = (m - 1) >> 5;
+            const uint32_t topb = 1u << ((m - 1) & 31);
+            const bool store_band = BAND && !full;
+            int amt_raw = m - n - 15 - q;  // band origin of column j = s-q+1
+            bool succ = false;
+            const int steps = in_dc ? n + G - 1 : 0;
+            uint32_t* trow = tab + d * WMAX;
+            uint32_t* grow = gtab + (int64_t)d * W * NW;
+            for (int s = 0; s < steps; ++s, ++amt_raw) {
+                const int j = s - q + 1;
+                uint32_t b[NW];
 #pragma unroll
-                                for (int w = 0; w < NW; ++w) b[w] = src[w];
-                            }
-                            uint32_t sv[NW], r[NW];
-                            shl1<NW>(v, sv);
-                            const uint32_t* pm = pmcol + (j - 1) * NW;
-                            if (d == 0) {
+                for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(gmask, outv[w], 1, G);
+                if (active && j >= 1 && j <= n) {
+                    if (q == 0 && d > 0) {
 #pragma unroll
-                                for (int w = 0; w < NW; ++w) r[w] = sv[w] | pm[w];
-                            } else {
-                                uint32_t tt[NW], st[NW];
-#pragma unroll
-                                for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
-                                shl1<NW>(tt, st);
-#pragma unroll
-                                for (int w = 0; w < NW; ++w) {
-                                    r[w] = (sv[w] | pm[w]) & st[w] & a[w];
-                                    a[w] = b[w];
-                                }
-                            }
-                            uint32_t* dst = entry(d, j);
-#pragma unroll
-                            for (int w = 0; w < NW; ++w) {
-                                dst[w] = r[w];
-                                v[w] = r[w];
-                                outv[w] = r[w];
-                            }
-                            if (j == n) succ = (word_sel<NW>(r, topw) & topb) == 0u;
-                        }
+                        for (int w = 0; w < NW; ++w) b[w] = carry[(j - 1) * NW + w];
                     }
-                    const unsigned bal = (__ballot_sync(gmask, succ) >> gbase) & lowmask;
-                    // the overflow writes of this pass must be visible to lane 0 of the next
-                    __syncwarp(gmask);
-                    if (bal) {
-                        d_min = pass * G + __ffs(bal) - 1;
-                        break;
+                    uint32_t tt[NW], st[NW], sv[NW], r[NW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
+                    shl1<NW>(tt, st);
+                    shl1<NW>(v, sv);
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        const uint32_t pm = pmcol[(j - 1) * NW + w];
+                        r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
+                        a[w] = b[w];
+                        v[w] = r[w];
+                        outv[w] = r[w];
                     }
+                    if (!BAND) {
+                        trow[j - 1] = r[0];
+                    } else if (store_band) {
+                        int amt = amt_raw < 0 ? 0 : amt_raw;
+                        amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
+                        trow[j - 1] = band32<NW>(r, amt);
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) grow[(j - 1) * NW + w] = r[w];
+                    }
+                    if (q == G - 1) {
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) carry[(j - 1) * NW + w] = r[w];
+                    }
+                    if (j == n) succ = (word_sel<NW>(r, topw) & topb) == 0u;
+#ifdef GA_DEBUG
+                    if (pair == 1) printf("DC d=%d j=%d r=%08x pm=%08x b=%08x\n", d, j, r[0],
+                                          pmcol[(j - 1) * NW], b[0]);
+#endif
                 }
             }
-            if (d_min < 0) {  // NotFound(k) -> WindowFailed(index, k) (window.py:108-109)
-                res.status = 1;
-                res.fail_window = widx;
-                break;
+            if (in_dc) {
+                const unsigned bal = (__ballot_sync(gmask, succ) >> gbase) & lowmask;
+                if (bal) {
+                    d_min = pass * G + __ffs(bal) - 1;
+                    phase = IN_TB;
+                } else if ((pass + 1) * G > K) {  // NotFound(k) -> WindowFailed(index, k)
+                    write_result(1, widx);
+                    phase = NEED_PAIR;
+                } else if (BAND && !full && (pass + 1) * G >= LV) {
+                    full = true;  // d_min > 15: the band cannot serve TB; redo full width
+                    pass = 0;
+                } else {
+                    ++pass;
+                }
             }
+        }
 
-            // ---- GenASM-TB (backtrace.py:113-160), lane 0 walks ----
-            int consumed = 0, tcons = 0, stuck = 0;
-            if (q == 0) {
-                int j = n, d = d_min, i = m - 1;
-                int64_t nops = res.ops_len;
+        // ================= TB round (groups whose window solved) =================
+        if (__any_sync(0xffffffffu, phase == IN_TB)) {
+            if (phase == IN_TB) {
+                __syncwarp(gmask);
+                int d = d_min, j = n, i = m - 1, consumed = 0, tcons = 0, wcost = 0;
+                int64_t wreads = 0;
+                bool stuck = false;
                 for (;;) {
-                    if (i < 0) break;
-                    if (consumed >= budget) break;
-                    if (j == 0) {
-                        if (i + 1 > d) { stuck = 1; break; }
+                    if (i < 0 || consumed >= budget) break;
+                    if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+                        if (i + 1 > d) {
+                            stuck = true;
+                            break;
+                        }
                         const int take = (i + 1 < budget - consumed) ? i + 1 : budget - consumed;
-                        for (int u = 0; u < take; ++u) ops[nops++] = 'I';
-                        res.cost += take;
+                        for (int u = q; u < take; u += G) ops[nops + u] = 'I';
+                        nops += take;
+                        wcost += take;
                         consumed += take;
                         i -= take;
                         break;
                     }
-                    const int tc = ct[j - 1];
-                    const bool sym_eq = tc < 4 && cp[i] == tc;
-                    bool m_ok;
-                    if (i == 0) m_ok = sym_eq;
-                    else if (j == 1) m_ok = sym_eq && (i - 1 < d);
-                    else m_ok = sym_eq && !bit_of(entry(d, j - 1), i - 1);
-                    res.entry_reads += (j - 1 >= 1);
-                    bool s_ok = false, d_ok = false, i_ok = false;
-                    if (d > 0) {
-                        if (j == 1) {
-                            s_ok = (i == 0) || (i - 1 < d - 1);
-                            d_ok = i < d - 1;
-                        } else {
-                            const uint32_t* e = entry(d - 1, j - 1);
-                            s_ok = (i == 0) || !bit_of(e, i - 1);
-                            d_ok = !bit_of(e, i);
-                            res.entry_reads += 1;
+                    // lane q evaluates the state q diagonal ('=') steps ahead
+                    const int jq = j - q, iq = i - q;
+                    int op = OP_STOP, rd = 0;
+                    if (iq >= 0 && consumed + q < budget && jq >= 1) {
+                        bool oob = false;
+                        const int tc = ct[jq - 1];
+                        const bool symeq = tc < 4 && cp[iq] == tc;
+                        bool mok;
+                        if (iq == 0) mok = symeq;
+                        else if (jq == 1) mok = symeq && (iq - 1 < d);
+                        else mok = symeq && !tbit(d, jq - 1, iq - 1, oob);
+                        rd = jq >= 2;
+                        bool sok = false, dok = false, iok = false;
+                        if (d > 0) {
+                            if (jq == 1) {
+                                sok = iq == 0 || iq - 1 < d - 1;
+                                dok = iq < d - 1;
+                            } else {
+                                sok = iq == 0 || !tbit(d - 1, jq - 1, iq - 1, oob);
+                                dok = !tbit(d - 1, jq - 1, iq, oob);
+                                rd += 1;
+                            }
+                            iok = iq == 0 || !tbit(d - 1, jq, iq - 1, oob);
+                            rd += 1;
                         }
-                        i_ok = (i == 0) || !bit_of(entry(d - 1, j), i - 1);
-                        res.entry_reads += 1;
-                    }
-                    int op = -1;
+                        op = OP_STUCK;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int id = (P.prio >> (2 * u)) & 3;
-                        const bool ok = id == 0 ? m_ok : id == 1 ? s_ok : id == 2 ? i_ok : d_ok;
-                        if (op < 0 && ok) op = id;
+                        for (int u = 3; u >= 0; --u) {
+                            const int id = (P.prio >> (2 * u)) & 3;
+                            const bool ok = id == OP_M ? mok : id == OP_S ? sok : id == OP_I ? iok : dok;
+                            if (ok) op = id;
+                        }
+                        if (oob) op = OP_STUCK;
                     }
-                    if (op == 0) {
-                        ops[nops++] = '='; --j; --i; ++consumed; ++tcons;
-                    } else if (op == 1) {
-                        ops[nops++] = 'X'; --j; --d; --i; ++consumed; ++tcons; ++res.cost;
-                    } else if (op == 2) {
-                        ops[nops++] = 'I'; --d; --i; ++consumed; ++res.cost;
-                    } else if (op == 3) {
-                        ops[nops++] = 'D'; --j; --d; ++tcons; ++res.cost;
-                    } else {
-                        stuck = 1;
+                    const unsigned nz = (__ballot_sync(gmask, op != OP_M) >> gbase) & lowmask;
+                    const int f = nz ? __ffs(nz) - 1 : G;
+#ifdef GA_DEBUG
+                    if (pair == 1)
+                        printf("TB q=%d state d=%d j=%d i=%d c=%d -> lane (jq=%d iq=%d) op=%d f=%d\n", q,
+                               d, j, i, consumed, jq, iq, op, f);
+#endif
+                    if (q < f) ops[nops + q] = '=';
+                    wreads += __reduce_add_sync(gmask, q < f ? (unsigned)rd : 0u);
+                    j -= f;
+                    i -= f;
+                    consumed += f;
+                    tcons += f;
+                    nops += f;
+                    if (f == G) continue;
+                    const int opf = __shfl_sync(gmask, op, f, G);
+                    const int rdf = __shfl_sync(gmask, rd, f, G);
+                    if (opf == OP_STOP) continue;
+                    if (opf == OP_STUCK) {
+                        stuck = true;
                         break;
                     }
+                    wreads += rdf;
+                    uint8_t ch;
+                    if (opf == OP_S) {
+                        ch = 'X'; --j; --d; --i; ++consumed; ++tcons;
+                    } else if (opf == OP_I) {
+                        ch = 'I'; --d; --i; ++consumed;
+                    } else {
+                        ch = 'D'; --j; --d; ++tcons;
+                    }
+                    ++wcost;
+                    if (q == 0) ops[nops] = ch;
+                    ++nops;
                 }
-                res.ops_len = nops;
-                dists[widx] = (uint8_t)d_min;
-                res.rows_computed += d_min + 1;
-                // entry_writes / words_allocated in closed form
-                int64_t wr = 0;
-                for (int dd = 0; dd <= d_min; ++dd) {
+                // entry_writes / words_allocated of this window in closed form
+                // (sum over stored columns per level, dptable.py:62-82, 156-171)
+                unsigned wr = 0;
+                for (int dd = q; dd <= d_min; dd += G) {
                     int ss = n - budget - (K - dd) - 1;
                     ss = ss > 1 ? ss : 1;
                     const int cnt = n - ss + 1;
-                    wr += cnt > 0 ? cnt : 0;
+                    wr += cnt > 0 ? (unsigned)cnt : 0u;
                 }
-                res.entry_writes += wr;
-                res.words_allocated += wr * ((m + 63) / 64);
+                wr = __reduce_add_sync(gmask, wr);
+                if (stuck) {
+                    write_result(3, widx);
+                    phase = NEED_PAIR;
+                } else {
+                    if (q == 0) {
+                        dists[widx] = (uint8_t)d_min;
+                        rows += d_min + 1;
+                        cost += wcost;
+                        reads += wreads;
+                        writes += wr;
+                        words += (int64_t)wr * ((m + 63) / 64);
+                    }
+                    p += consumed;
+                    t += tcons;
+                    ++widx;
+                    if (p < Lp) {
+                        phase = NEED_WINDOW;
+                    } else {
+                        write_result(0, -1);
+                        phase = NEED_PAIR;
+                    }
+                }
             }
-            consumed = __shfl_sync(gmask, consumed, 0, G);
-            tcons = __shfl_sync(gmask, tcons, 0, G);
-            stuck = __shfl_sync(gmask, stuck, 0, G);
-            if (stuck) {
-                res.status = 3;
-                res.fail_window = widx;
-                break;
-            }
-            p += consumed;
-            t += tcons;
-            ++widx;
-        }
-        if (q == 0) {
-            res.text_consumed = t;
-            if (res.status != 0) {  // a failed slot carries only its error (window.py:144-149)
-                const int32_t st = res.status, fw = res.fail_window;
-                res = PairResult{};
-                res.status = st;
-                res.fail_window = fw;
-            }
-            results[pair] = res;
         }
     }
 }
@@ -320,75 +445,62 @@ genasm_window_kernel(const KernelParams P) {
 // ---------------------------------------------------------------------------
 
 template <int NW, int G>
-static cudaError_t launch_t(const KernelParams& base, int s_lv, int smem_budget, int num_sms,
-                            cudaStream_t stream,
+static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cudaStream_t stream,
                             uint32_t** overflow, size_t* overflow_cap, LaunchShape* shape) {
-    constexpr int WMAX = 32 * NW;
+    using GE = Geo<NW>;
     KernelParams P = base;
-    const int groups_per_block = kBlockThreads / G;
-    // shared-memory table depth: requested levels, capped so one block fits
-    // in the per-block budget (GA_SMEM_KB) -- deeper levels use the overflow
-    const int levels_cap = ((P.k + 1 + G - 1) / G) * G;
-    const int fixed_words = WMAX * NW + WMAX / 2;
-    const int level_words = P.W * NW;
-    const int fit = (smem_budget / 4 / groups_per_block - fixed_words) / level_words;
-    if (s_lv > fit) s_lv = fit;
-    if (s_lv > levels_cap) s_lv = levels_cap;
-    if (s_lv < 0) s_lv = 0;
-    P.s_lv = s_lv;
-    const int group_words = s_lv * P.W * NW + WMAX * NW + WMAX / 2;
-    const int smem = groups_per_block * group_words * 4;
-    auto kern = genasm_window_kernel<NW, G>;
+    if (block < G || block > kMaxBlock || block % 32) block = 64;
+    const int groups_per_block = block / G;
+    const int smem = groups_per_block * GE::GROUP_W * 4;
+    auto kern = genasm_kernel<NW, G>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlockThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    int64_t groups_needed = (P.n_pairs + 0);
     int grid = num_sms * per_sm;
-    const int64_t max_useful = (groups_needed + groups_per_block - 1) / groups_per_block;
+    const int64_t max_useful = (P.n_pairs + groups_per_block - 1) / groups_per_block;
     if (grid > max_useful) grid = (int)(max_useful > 0 ? max_useful : 1);
-    const int64_t ovf_levels = levels_cap > s_lv ? levels_cap - s_lv : 0;
-    P.overflow_words_per_group = ovf_levels * P.W * NW;
+    const int levels_cap = ((P.k + 1 + G - 1) / G) * G;
+    P.overflow_words_per_group = GE::BAND ? (int64_t)levels_cap * P.W * NW : 0;
     const size_t need = (size_t)grid * groups_per_block * (size_t)P.overflow_words_per_group;
-    if (need > *overflow_cap) {
+    if (need > *overflow_cap || !*overflow) {
         if (*overflow) cudaFree(*overflow);
         *overflow = nullptr;
         *overflow_cap = 0;
-        e = cudaMalloc(overflow, need * 4 + 16);
+        e = cudaMalloc(overflow, need * 4 + 64);
         if (e != cudaSuccess) return e;
         *overflow_cap = need;
     }
     P.overflow = *overflow;
-    kern<<<grid, kBlockThreads, smem, stream>>>(P);
+    kern<<<grid, block, smem, stream>>>(P);
     shape->grid = grid;
-    shape->block = kBlockThreads;
+    shape->block = block;
     shape->smem_bytes = smem;
-    shape->s_lv = s_lv;
     shape->group = G;
+    shape->blocks_per_sm = per_sm;
     shape->overflow_words_per_group = P.overflow_words_per_group;
     return cudaGetLastError();
 }
 
 template <int NW>
-static cudaError_t launch_nw(const KernelParams& P, int group, int s_lv, int sb, int num_sms,
+static cudaError_t launch_nw(const KernelParams& P, int group, int block, int num_sms,
                              cudaStream_t stream, uint32_t** overflow, size_t* cap,
                              LaunchShape* shape) {
     switch (group) {
-        case 8: return launch_t<NW, 8>(P, s_lv, sb, num_sms, stream, overflow, cap, shape);
-        case 16: return launch_t<NW, 16>(P, s_lv, sb, num_sms, stream, overflow, cap, shape);
-        case 32: return launch_t<NW, 32>(P, s_lv, sb, num_sms, stream, overflow, cap, shape);
+        case 8: return launch_t<NW, 8>(P, block, num_sms, stream, overflow, cap, shape);
+        case 16: return launch_t<NW, 16>(P, block, num_sms, stream, overflow, cap, shape);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_genasm(const KernelParams& P, int group, int s_lv, int sb, int num_sms,
+cudaError_t launch_genasm(const KernelParams& P, int group, int block, int num_sms,
                           cudaStream_t stream, uint32_t** overflow, size_t* cap,
                           LaunchShape* shape) {
-    if (P.W <= 32) return launch_nw<1>(P, group, s_lv, sb, num_sms, stream, overflow, cap, shape);
-    if (P.W <= 64) return launch_nw<2>(P, group, s_lv, sb, num_sms, stream, overflow, cap, shape);
-    if (P.W <= 128) return launch_nw<4>(P, group, s_lv, sb, num_sms, stream, overflow, cap, shape);
+    if (P.W <= 32) return launch_nw<1>(P, group, block, num_sms, stream, overflow, cap, shape);
+    if (P.W <= 64) return launch_nw<2>(P, group, block, num_sms, stream, overflow, cap, shape);
+    if (P.W <= 128) return launch_nw<4>(P, group, block, num_sms, stream, overflow, cap, shape);
     return cudaErrorInvalidValue;
 }
 

@@ -1,27 +1,42 @@
 // genasm_kernel.cuh -- fused windowed GenASM-DC + GenASM-TB for sm_100a.
 //
-// One pair per GROUP of G lanes (G = 8/16/32; 32/G pairs per warp).  A
-// persistent grid pulls pairs from an atomic queue in longest-first order.
-// Per pair the lanes walk the reference's sequential window chain
-// (pkg/src/bitalign/window.py:95-120); per window:
+// Work mapping.  A persistent grid; every warp holds 32/G pairs, one per GROUP
+// of G consecutive lanes (G = 8 by default).  Groups pull pairs from an atomic
+// queue (longest first) and walk the reference's sequential window chain
+// (pkg/src/bitalign/window.py:95-120).  The groups of a warp advance in
+// PASS ROUNDS: every round, every group runs one DC pass of its current
+// window in lock-step (no divergence on the hot loop); groups whose window
+// solved in that pass then trace back together, set up their next window (or
+// pull the next pair) and rejoin at the next round.
 //
-//   DC (pkg/src/bitalign/distance.py:97-150): levels-as-lanes wavefront.
-//     Pass p evaluates levels pG..pG+G-1, lane q owns level d = pG+q and at
-//     step s computes column j = s-q+1, receiving R[d-1][j] from lane q-1
-//     by one warp shuffle (lane 0 reads level pG-1 back from the table).
-//     Rows are NW x 32-bit registers (W <= 32*NW).  Early termination (key
-//     idea 2): the first pass containing a level whose column-n row has bit
-//     m-1 clear ends the DC; d_min is the lowest such level.  The table
-//     keeps exactly one status row per entry, the AND of the four edges
+//   DC pass (pkg/src/bitalign/distance.py:97-150): levels-as-lanes wavefront.
+//     Pass p evaluates levels pG..pG+G-1; lane q owns level d = pG+q and at
+//     step s computes column j = s-q+1, receiving R[d-1][j] from lane q-1 by
+//     one warp shuffle.  Lane 0 reads level pG-1 from the group's carry row
+//     (full-width rows of the previous pass's last level).  Rows are NW x 32-bit
+//     registers (W <= 32 NW).  Early termination (key idea 2): the window ends
+//     at the first pass holding a level whose column-n row has bit m-1 clear.
+//     The table keeps one status row per entry -- the AND of the four edges
 //     (key idea 1).
-//   TB (pkg/src/bitalign/backtrace.py:70-167): greedy walk from
-//     (j=n, d=d_min, i=m-1), edge bits recomputed from three table reads
-//     (backtrace.py:84-99) and the symbol codes, first active edge in the
-//     configured priority.  Ops are emitted in walk (= forward) order.
 //
-// Table placement: levels < S_LV live in shared memory, the rest in a
-// per-group global overflow slab.  Counters follow the reference's stored
-// predicate (dptable.py:62-82) in closed form.
+//   Table (key idea 3, extended to bits).  A traceback state (d, j, i) on any
+//     path from (d_min, n, m-1) satisfies |(m-1-i) - (n-j)| <= d_min - d, so
+//     every table read of entry (e, j) touches bits within d_min - e of the
+//     diagonal c_j = m-1-n+j.  When d_min <= 15 a 32-bit band around c_j holds
+//     every bit the traceback can ever read: band mode stores 32 bits per
+//     entry for levels 0..15 in shared memory.  A window needing level 16+
+//     restarts in full mode (full-width rows in a per-group global slab).
+//     W <= 32 rows are 32 bits wide and always live in shared memory.
+//
+//   TB (pkg/src/bitalign/backtrace.py:70-167): greedy walk from
+//     (j=n, d=d_min, i=m-1), edge bits recomputed from three table reads and
+//     the symbol codes (backtrace.py:84-99), first active edge in the
+//     configured priority.  The G lanes speculate G consecutive diagonal
+//     ('=') steps at once; a ballot finds the first non-match, so a run of
+//     matches costs one round trip.  Ops are emitted in walk (= forward) order.
+//
+// Counters follow the reference's stored predicate (dptable.py:62-82) in
+// closed form; entry reads are counted per taken step.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,9 +58,8 @@ struct KernelParams {
     uint8_t* ops;
     const int64_t* win_off;
     uint8_t* dists;
-    uint32_t* overflow;        // per-group global table slabs
+    uint32_t* overflow;        // per-group global full-mode table slabs
     int64_t overflow_words_per_group;
-    int32_t s_lv;              // table levels resident in shared memory
     unsigned long long* queue; // atomic pair counter
 };
 
@@ -55,11 +69,11 @@ struct PairResult {  // == ga_pair_result
 };
 
 struct LaunchShape {
-    int grid, block, smem_bytes, s_lv, group;
+    int grid, block, smem_bytes, group, blocks_per_sm;
     int64_t overflow_words_per_group;
 };
 
-cudaError_t launch_genasm(const KernelParams& P, int group, int s_lv, int smem_budget, int num_sms,
+cudaError_t launch_genasm(const KernelParams& P, int group, int block_threads, int num_sms,
                           cudaStream_t stream, uint32_t** overflow, size_t* cap,
                           LaunchShape* shape);
 

@@ -19,7 +19,7 @@ from . import _abi
 from ._abi import PackedBatch, PackedResults
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_genasm.so")
+SO_PATH = os.environ.get("GA_SO") or os.path.join(_HERE, "_genasm.so")
 
 _lib = None
 _lib_lock = threading.Lock()

@@ -109,8 +109,9 @@ def test_lpt_split_balances_and_partitions():
 
 
 def _header_functions():
-    text = "".join(open(os.path.join(ROOT, "include", h)).read()
-                   for h in ("genasm.h", "genasm_sim.h"))
+    inc = os.path.join(ROOT, "include")
+    text = "".join(open(os.path.join(inc, h)).read()
+                   for h in sorted(os.listdir(inc)) if h.endswith(".h"))
     return sorted(set(re.findall(r"\b(ga_[a-z0-9_]+)\s*\(", text)))
 
 
