@@ -67,6 +67,95 @@ struct Geo {
     static constexpr int BAND_MAX = 32 * NW - 32;
 };
 
+// One lane of the DC wavefront: level d = pass*G + q; at step s it evaluates
+// column j = s-q+1 of R[d] (distance.py:125-149), receiving R[d-1][j] from
+// lane q-1 by shuffle (lane 0: the carry row of the previous pass).
+// PRED: fill/drain steps where some lanes are outside [1, n]; MIXED: some
+// group of the warp stores full-width rows (full mode) this round.
+template <int NW, int G>
+struct DcLane {
+    using GE = Geo<NW>;
+    uint32_t v[NW], a[NW], outv[NW];
+    uint32_t lvl0;
+    int q, n, amt_base;
+    bool active, lane0carry, lastlane, full;
+    uint32_t* trow;
+    uint32_t* grow;
+    uint32_t* crow;
+    const uint32_t* prow;
+
+    __device__ __forceinline__ void init(int q_, bool in_dc, int pass, int m, int n_, int K, int W,
+                                         bool full_, uint32_t* tab, uint32_t* carry,
+                                         const uint32_t* pmcol, uint32_t* gtab) {
+        q = q_;
+        n = n_;
+        const int d = pass * G + q;
+        active = in_dc && d <= K;
+        lane0carry = active && q == 0 && d > 0;
+        lastlane = active && q == G - 1;
+        full = full_;
+        init_row<NW>(v, m, d);                // R[d][0] = init(m, d)
+        init_row<NW>(a, m, d > 0 ? d - 1 : 0);  // R[d-1][0]
+        lvl0 = d == 0 ? 0xffffffffu : 0u;     // level 0 has only the match edge
+#pragma unroll
+        for (int w = 0; w < NW; ++w) outv[w] = 0u;
+        amt_base = m - n - 15 - q;            // band origin of column j = s-q+1
+        const int dd = d < GE::LV ? d : 0;
+        trow = tab + dd * GE::WMAX;
+        grow = gtab + (int64_t)d * W * NW;
+        crow = carry;
+        prow = pmcol;
+    }
+
+    template <bool PRED, bool MIXED>
+    __device__ __forceinline__ void step(int s) {
+        uint32_t b[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
+        const int c = s - q;  // column j-1
+        const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
+        if (lane0carry && (!PRED || inr)) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) b[w] = crow[c * NW + w];
+        }
+        uint32_t tt[NW], st[NW], sv[NW], r[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
+        shl1<NW>(tt, st);
+        shl1<NW>(v, sv);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t pm = prow[c * NW + w];
+            r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
+        }
+        if (!PRED || inr) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                a[w] = b[w];
+                v[w] = r[w];
+                outv[w] = r[w];
+            }
+        }
+        if (inr) {
+            if (!GE::BAND) {
+                trow[c] = r[0];
+            } else if (MIXED && full) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) grow[c * NW + w] = r[w];
+            } else {
+                int amt = amt_base + s;
+                amt = amt < 0 ? 0 : amt;
+                if (NW > 2) amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
+                trow[c] = band32<NW>(r, amt);
+            }
+        }
+        if (lastlane && (!PRED || inr)) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) crow[c * NW + w] = r[w];
+        }
+    }
+};
+
 template <int NW, int G>
 __global__ void __launch_bounds__(kMaxBlock)
 genasm_kernel(const KernelParams P) {
@@ -233,70 +322,25 @@ genasm_kernel(const KernelParams P) {
         // ================= DC pass round (all groups in lock-step) =================
         {
             const bool in_dc = phase == IN_DC;
-            const int d = pass * G + q;
-            const bool active = in_dc && d <= K;
-            uint32_t v[NW], a[NW], outv[NW];
-            init_row<NW>(v, m, d);
-            init_row<NW>(a, m, d > 0 ? d - 1 : 0);
-            const uint32_t lvl0 = d == 0 ? 0xffffffffu : 0u;  // level 0 has only the M edge
-            if (d == 0) {
-#pragma unroll
-                for (int w = 0; w < NW; ++w) a[w] = 0xffffffffu;
+            DcLane<NW, G> L;
+            L.init(q, in_dc, pass, m, n, K, W, full, tab, carry, pmcol, gtab);
+            // warp-uniform trip counts: fill [0, G-1), steady [G-1, nmin), drain [.., steps)
+            const int steps = __reduce_max_sync(0xffffffffu, in_dc ? n + G - 1 : 0);
+            const int nmin = __reduce_min_sync(0xffffffffu, in_dc ? n : WMAX);
+            const int fill_end = steps < G - 1 ? steps : G - 1;
+            const int steady_end = nmin > fill_end ? nmin : fill_end;
+            if (BAND && __any_sync(0xffffffffu, in_dc && full)) {
+                for (int s = 0; s < fill_end; ++s) L.template step<true, true>(s);
+                for (int s = fill_end; s < steady_end; ++s) L.template step<false, true>(s);
+                for (int s = steady_end; s < steps; ++s) L.template step<true, true>(s);
+            } else {
+                for (int s = 0; s < fill_end; ++s) L.template step<true, false>(s);
+#pragma unroll 4
+                for (int s = fill_end; s < steady_end; ++s) L.template step<false, false>(s);
+                for (int s = steady_end; s < steps; ++s) L.template step<true, false>(s);
             }
-#pragma unroll
-            for (int w = 0; w < NW; ++w) outv[w] = 0u;
-            const int topw = (m - 1) >> 5;
-            const uint32_t topb = 1u << ((m - 1) & 31);
-            const bool store_band = BAND && !full;
-            int amt_raw = m - n - 15 - q;  // band origin of column j = s-q+1
-            bool succ = false;
-            const int steps = in_dc ? n + G - 1 : 0;
-            uint32_t* trow = tab + d * WMAX;
-            uint32_t* grow = gtab + (int64_t)d * W * NW;
-            for (int s = 0; s < steps; ++s, ++amt_raw) {
-                const int j = s - q + 1;
-                uint32_t b[NW];
-#pragma unroll
-                for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(gmask, outv[w], 1, G);
-                if (active && j >= 1 && j <= n) {
-                    if (q == 0 && d > 0) {
-#pragma unroll
-                        for (int w = 0; w < NW; ++w) b[w] = carry[(j - 1) * NW + w];
-                    }
-                    uint32_t tt[NW], st[NW], sv[NW], r[NW];
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
-                    shl1<NW>(tt, st);
-                    shl1<NW>(v, sv);
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        const uint32_t pm = pmcol[(j - 1) * NW + w];
-                        r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
-                        a[w] = b[w];
-                        v[w] = r[w];
-                        outv[w] = r[w];
-                    }
-                    if (!BAND) {
-                        trow[j - 1] = r[0];
-                    } else if (store_band) {
-                        int amt = amt_raw < 0 ? 0 : amt_raw;
-                        amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
-                        trow[j - 1] = band32<NW>(r, amt);
-                    } else {
-#pragma unroll
-                        for (int w = 0; w < NW; ++w) grow[(j - 1) * NW + w] = r[w];
-                    }
-                    if (q == G - 1) {
-#pragma unroll
-                        for (int w = 0; w < NW; ++w) carry[(j - 1) * NW + w] = r[w];
-                    }
-                    if (j == n) succ = (word_sel<NW>(r, topw) & topb) == 0u;
-#ifdef GA_DEBUG
-                    if (pair == 1) printf("DC d=%d j=%d r=%08x pm=%08x b=%08x\n", d, j, r[0],
-                                          pmcol[(j - 1) * NW], b[0]);
-#endif
-                }
-            }
+            const bool succ = L.active && n >= 1 &&
+                              (word_sel<NW>(L.v, (m - 1) >> 5) & (1u << ((m - 1) & 31))) == 0u;
             if (in_dc) {
                 const unsigned bal = (__ballot_sync(gmask, succ) >> gbase) & lowmask;
                 if (bal) {
