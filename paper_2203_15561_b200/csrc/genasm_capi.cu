@@ -207,6 +207,16 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     P.O = cfg->overlap;
     P.k = cfg->k;
     P.prio = pack_priority(cfg->priority);
+    // first active edge in priority order (backtrace.py:134-160); 5 = none (stuck)
+    P.prio_lut = 0;
+    for (uint64_t mask = 0; mask < 16; ++mask) {
+        uint64_t op = 5;
+        for (int u = 3; u >= 0; --u) {
+            const uint64_t id = (P.prio >> (2 * u)) & 3u;
+            if (mask & (1ull << id)) op = id;
+        }
+        P.prio_lut |= op << (4 * mask);
+    }
     P.results = out->results;
     P.ops_off = out->ops_off;
     P.ops = out->ops;

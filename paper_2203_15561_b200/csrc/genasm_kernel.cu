@@ -114,7 +114,15 @@ struct DcLane {
         for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
         const int c = s - q;  // column j-1
         const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
-        if (lane0carry && (!PRED || inr)) {
+        if (PRED) {
+            // branch-free fill/drain: every c in [-(G-1), n+G-2] addresses words
+            // inside this group's shared region, so the loads need no guard
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t cw = crow[c * NW + w];
+                b[w] = lane0carry ? cw : b[w];
+            }
+        } else if (lane0carry) {
 #pragma unroll
             for (int w = 0; w < NW; ++w) b[w] = crow[c * NW + w];
         }
@@ -128,13 +136,11 @@ struct DcLane {
             const uint32_t pm = prow[c * NW + w];
             r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
         }
-        if (!PRED || inr) {
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                a[w] = b[w];
-                v[w] = r[w];
-                outv[w] = r[w];
-            }
+        for (int w = 0; w < NW; ++w) {
+            a[w] = PRED ? (inr ? b[w] : a[w]) : b[w];
+            v[w] = PRED ? (inr ? r[w] : v[w]) : r[w];
+            outv[w] = PRED ? (inr ? r[w] : outv[w]) : r[w];
         }
         if (inr) {
             if (!GE::BAND) {
@@ -149,12 +155,28 @@ struct DcLane {
                 trow[c] = band32<NW>(r, amt);
             }
         }
-        if (lastlane && (!PRED || inr)) {
+        if (lastlane && inr) {
 #pragma unroll
             for (int w = 0; w < NW; ++w) crow[c * NW + w] = r[w];
         }
     }
 };
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// reductions over the G lanes of a group, all 32 lanes participating
+template <int G>
+__device__ __forceinline__ unsigned group_sum(unsigned x) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o, G);
+    return x;
+}
+template <int G>
+__device__ __forceinline__ unsigned group_or(unsigned x) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) x |= __shfl_xor_sync(FULL, x, o, G);
+    return x;
+}
 
 template <int NW, int G>
 __global__ void __launch_bounds__(kMaxBlock)
@@ -167,8 +189,7 @@ genasm_kernel(const KernelParams P) {
     const int lane = threadIdx.x & 31;
     const int q = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
-    const unsigned lowmask = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
+    const unsigned lowmask = (G == 32) ? FULL : ((1u << G) - 1u);
     const int gib = threadIdx.x / G;
     const int groups_per_block = blockDim.x / G;
 
@@ -214,110 +235,101 @@ genasm_kernel(const KernelParams P) {
         }
     };
 
-    // bit x of table entry (e, col), col >= 1; sets oob if outside the stored band
-    auto tbit = [&](int e, int col, int x, bool& oob) -> uint32_t {
-        if (BAND && full) {
-            const uint32_t* row = gtab + ((int64_t)e * W + (col - 1)) * NW;
-            return (row[x >> 5] >> (x & 31)) & 1u;
-        }
-        const uint32_t word = tab[e * WMAX + (col - 1)];
-        if (!BAND) return (word >> x) & 1u;
-        int amt = m - 1 - n + col - 15;
-        amt = amt < 0 ? 0 : (amt > GE::BAND_MAX ? GE::BAND_MAX : amt);
-        const int rel = x - amt;
-        if (rel < 0 || rel > 31) {
-            oob = true;
-            return 1u;
-        }
-        return (word >> rel) & 1u;
-    };
-
     for (;;) {
-        // ================= setup: next pair / next window =================
-        while (phase == NEED_PAIR || phase == NEED_WINDOW) {
-            if (phase == NEED_PAIR) {
-                unsigned long long idx = 0;
-                if (q == 0) idx = atomicAdd(P.queue, 1ull);
-                idx = __shfl_sync(gmask, idx, 0, G);
+        // ================= next pair (empty patterns are settled here) =================
+        while (__any_sync(FULL, phase == NEED_PAIR)) {
+            const bool need = phase == NEED_PAIR;
+            unsigned long long idx = 0;
+            if (need && q == 0) idx = atomicAdd(P.queue, 1ull);
+            idx = __shfl_sync(FULL, idx, 0, G);
+            if (need) {
                 if (idx >= (unsigned long long)P.n_pairs) {
                     phase = DONE;
-                    break;
+                } else {
+                    pair = P.order ? (int64_t)P.order[idx] : (int64_t)idx;
+                    Lp = P.pat_len[pair];
+                    Lt = P.txt_len[pair];
+                    Pp = P.codes + P.pat_off[pair];
+                    Tp = P.codes + P.txt_off[pair];
+                    ops = P.ops + P.ops_off[pair];
+                    dists = P.dists + P.win_off[pair];
+                    p = t = nops = 0;
+                    widx = 0;
+                    cost = rows = reads = writes = words = 0;
+                    if (Lp <= 0) write_result(2, -1);  // EmptyPattern (window.py:87-88)
+                    else phase = NEED_WINDOW;
                 }
-                pair = P.order ? (int64_t)P.order[idx] : (int64_t)idx;
-                Lp = P.pat_len[pair];
-                Lt = P.txt_len[pair];
-                Pp = P.codes + P.pat_off[pair];
-                Tp = P.codes + P.txt_off[pair];
-                ops = P.ops + P.ops_off[pair];
-                dists = P.dists + P.win_off[pair];
-                p = t = nops = 0;
-                widx = 0;
-                cost = rows = reads = writes = words = 0;
-                if (Lp <= 0) {  // EmptyPattern (window.py:87-88)
-                    write_result(2, -1);
-                    continue;
-                }
-                phase = NEED_WINDOW;
             }
-            // ---- window geometry (window.py:96-101) ----
-            const int64_t remaining = Lp - p;
-            const bool final_w = remaining <= W;
-            m = final_w ? (int)remaining : W;
-            const int64_t tleft = Lt - t;
-            n = tleft < W ? (int)(tleft > 0 ? tleft : 0) : W;
-            budget = final_w ? m : W - O;
-            // ---- reversed chunks (window.py:99-100) ----
-            __syncwarp(gmask);
-            for (int i = q; i < m; i += G) cp[i] = Pp[p + m - 1 - i];
-            for (int j = q; j < n; j += G) ct[j] = Tp[t + n - 1 - j];
-            __syncwarp(gmask);
-            // ---- pattern masks (distance.py:70-79), per-column masks (:91-94) ----
+        }
+        if (__all_sync(FULL, phase == DONE)) break;
+
+        // ================= next window: geometry, chunks, masks =================
+        if (__any_sync(FULL, phase == NEED_WINDOW)) {
+            const bool need = phase == NEED_WINDOW;
+            if (need) {
+                // window geometry (window.py:96-101)
+                const int64_t remaining = Lp - p;
+                const bool final_w = remaining <= W;
+                m = final_w ? (int)remaining : W;
+                const int64_t tleft = Lt - t;
+                n = tleft < W ? (int)(tleft > 0 ? tleft : 0) : W;
+                budget = final_w ? m : W - O;
+                // reversed chunks (window.py:99-100)
+                for (int i = q; i < m; i += G) cp[i] = Pp[p + m - 1 - i];
+                for (int j = q; j < n; j += G) ct[j] = Tp[t + n - 1 - j];
+            }
+            __syncwarp();
+            // pattern masks (distance.py:70-79): match bits per symbol, OR-reduced
             uint32_t mt[4][NW];
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
                 for (int w = 0; w < NW; ++w) mt[c][w] = 0u;
-            for (int i = q; i < m; i += G) {
-                const int c = cp[i];
-                const uint32_t bit = 1u << (i & 31);
-                const int wi = i >> 5;
+            if (need) {
+                for (int i = q; i < m; i += G) {
+                    const int c = cp[i];
+                    const uint32_t bit = 1u << (i & 31);
+                    const int wi = i >> 5;
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc)
+                    for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) mt[cc][w] |= (c == cc && wi == w) ? bit : 0u;
+                        for (int w = 0; w < NW; ++w) mt[cc][w] |= (c == cc && wi == w) ? bit : 0u;
+                }
             }
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-                for (int w = 0; w < NW; ++w) mt[cc][w] = ~__reduce_or_sync(gmask, mt[cc][w]);
-            for (int j = q; j < n; j += G) {
-                const int c = ct[j];
+                for (int w = 0; w < NW; ++w) mt[cc][w] = ~group_or<G>(mt[cc][w]);
+            if (need) {
+                // per-column masks (distance.py:91-94): PM[T[j-1]], all-ones off the alphabet
+                for (int j = q; j < n; j += G) {
+                    const int c = ct[j];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    uint32_t x = 0xffffffffu;
-                    x = (c == 0) ? mt[0][w] : x;
-                    x = (c == 1) ? mt[1][w] : x;
-                    x = (c == 2) ? mt[2][w] : x;
-                    x = (c == 3) ? mt[3][w] : x;
-                    pmcol[j * NW + w] = x;
+                    for (int w = 0; w < NW; ++w) {
+                        uint32_t x = 0xffffffffu;
+                        x = (c == 0) ? mt[0][w] : x;
+                        x = (c == 1) ? mt[1][w] : x;
+                        x = (c == 2) ? mt[2][w] : x;
+                        x = (c == 3) ? mt[3][w] : x;
+                        pmcol[j * NW + w] = x;
+                    }
                 }
-            }
-            pass = 0;
-            full = false;
-            if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
-                if (m <= K) {
-                    d_min = m;
-                    phase = IN_TB;
+                pass = 0;
+                full = false;
+                if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
+                    if (m <= K) {
+                        d_min = m;
+                        phase = IN_TB;
+                    } else {
+                        write_result(1, widx);
+                        phase = NEED_PAIR;
+                    }
                 } else {
-                    write_result(1, widx);
-                    phase = NEED_PAIR;
+                    phase = IN_DC;
                 }
-            } else {
-                phase = IN_DC;
             }
+            __syncwarp();
         }
-        if (__all_sync(0xffffffffu, phase == DONE)) break;
-        __syncwarp();
 
         // ================= DC pass round (all groups in lock-step) =================
         {
@@ -325,11 +337,11 @@ genasm_kernel(const KernelParams P) {
             DcLane<NW, G> L;
             L.init(q, in_dc, pass, m, n, K, W, full, tab, carry, pmcol, gtab);
             // warp-uniform trip counts: fill [0, G-1), steady [G-1, nmin), drain [.., steps)
-            const int steps = __reduce_max_sync(0xffffffffu, in_dc ? n + G - 1 : 0);
-            const int nmin = __reduce_min_sync(0xffffffffu, in_dc ? n : WMAX);
+            const int steps = __reduce_max_sync(FULL, in_dc ? n + G - 1 : 0);
+            const int nmin = __reduce_min_sync(FULL, in_dc ? n : WMAX);
             const int fill_end = steps < G - 1 ? steps : G - 1;
             const int steady_end = nmin > fill_end ? nmin : fill_end;
-            if (BAND && __any_sync(0xffffffffu, in_dc && full)) {
+            if (BAND && __any_sync(FULL, in_dc && full)) {
                 for (int s = 0; s < fill_end; ++s) L.template step<true, true>(s);
                 for (int s = fill_end; s < steady_end; ++s) L.template step<false, true>(s);
                 for (int s = steady_end; s < steps; ++s) L.template step<true, true>(s);
@@ -341,8 +353,8 @@ genasm_kernel(const KernelParams P) {
             }
             const bool succ = L.active && n >= 1 &&
                               (word_sel<NW>(L.v, (m - 1) >> 5) & (1u << ((m - 1) & 31))) == 0u;
+            const unsigned bal = (__ballot_sync(FULL, succ) >> gbase) & lowmask;
             if (in_dc) {
-                const unsigned bal = (__ballot_sync(gmask, succ) >> gbase) & lowmask;
                 if (bal) {
                     d_min = pass * G + __ffs(bal) - 1;
                     phase = IN_TB;
@@ -359,106 +371,129 @@ genasm_kernel(const KernelParams P) {
         }
 
         // ================= TB round (groups whose window solved) =================
-        if (__any_sync(0xffffffffu, phase == IN_TB)) {
-            if (phase == IN_TB) {
-                __syncwarp(gmask);
-                int d = d_min, j = n, i = m - 1, consumed = 0, tcons = 0, wcost = 0;
-                int64_t wreads = 0;
-                bool stuck = false;
-                for (;;) {
-                    if (i < 0 || consumed >= budget) break;
-                    if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+        if (__any_sync(FULL, phase == IN_TB)) {
+            __syncwarp();
+            const bool tbg = phase == IN_TB;
+            int d = d_min, j = n, i = m - 1, consumed = 0, tcons = 0, wcost = 0;
+            unsigned lreads = 0;
+            bool stuck = false, going = tbg;
+            const int cbase = m - 1 - n - 15;  // band origin of column col: cbase + col, clamped
+            for (;;) {
+                if (going) {
+                    if (i < 0 || consumed >= budget) {
+                        going = false;
+                    } else if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
                         if (i + 1 > d) {
                             stuck = true;
-                            break;
+                        } else {
+                            const int take = (i + 1 < budget - consumed) ? i + 1 : budget - consumed;
+                            for (int u = q; u < take; u += G) ops[nops + u] = 'I';
+                            nops += take;
+                            wcost += take;
+                            consumed += take;
+                            i -= take;
                         }
-                        const int take = (i + 1 < budget - consumed) ? i + 1 : budget - consumed;
-                        for (int u = q; u < take; u += G) ops[nops + u] = 'I';
-                        nops += take;
-                        wcost += take;
-                        consumed += take;
-                        i -= take;
-                        break;
+                        going = false;
                     }
-                    // lane q evaluates the state q diagonal ('=') steps ahead
-                    const int jq = j - q, iq = i - q;
-                    int op = OP_STOP, rd = 0;
-                    if (iq >= 0 && consumed + q < budget && jq >= 1) {
-                        bool oob = false;
-                        const int tc = ct[jq - 1];
-                        const bool symeq = tc < 4 && cp[iq] == tc;
-                        bool mok;
-                        if (iq == 0) mok = symeq;
-                        else if (jq == 1) mok = symeq && (iq - 1 < d);
-                        else mok = symeq && !tbit(d, jq - 1, iq - 1, oob);
-                        rd = jq >= 2;
-                        bool sok = false, dok = false, iok = false;
-                        if (d > 0) {
-                            if (jq == 1) {
-                                sok = iq == 0 || iq - 1 < d - 1;
-                                dok = iq < d - 1;
-                            } else {
-                                sok = iq == 0 || !tbit(d - 1, jq - 1, iq - 1, oob);
-                                dok = !tbit(d - 1, jq - 1, iq, oob);
-                                rd += 1;
-                            }
-                            iok = iq == 0 || !tbit(d - 1, jq, iq - 1, oob);
-                            rd += 1;
-                        }
-                        op = OP_STUCK;
-#pragma unroll
-                        for (int u = 3; u >= 0; --u) {
-                            const int id = (P.prio >> (2 * u)) & 3;
-                            const bool ok = id == OP_M ? mok : id == OP_S ? sok : id == OP_I ? iok : dok;
-                            if (ok) op = id;
-                        }
-                        if (oob) op = OP_STUCK;
+                }
+                if (!__any_sync(FULL, going)) break;
+                // lane q evaluates the state q diagonal ('=') steps ahead (backtrace.py:88-99)
+                const int jq = j - q, iq = i - q;
+                int op = OP_STOP;
+                unsigned rd = 0;
+                if (going && iq >= 0 && consumed + q < budget && jq >= 1) {
+                    const int tcode = ct[jq - 1];
+                    const bool symeq = tcode < 4 && cp[iq] == tcode;
+                    const int dm1 = d > 0 ? d - 1 : 0;
+                    const int col1 = jq - 1;
+                    uint32_t mb, sb, db, ib;  // table bits, 1 = inactive
+                    if (BAND && full) {
+                        auto gbit = [&](int e, int col, int x) -> uint32_t {
+                            col = col > 1 ? col : 1;
+                            x = x > 0 ? x : 0;
+                            const uint32_t* row = gtab + ((int64_t)e * W + (col - 1)) * NW;
+                            return row[x >> 5] >> (x & 31);
+                        };
+                        mb = gbit(d, col1, iq - 1);
+                        sb = gbit(dm1, col1, iq - 1);
+                        db = gbit(dm1, col1, iq);
+                        ib = gbit(dm1, jq, iq - 1);
+                    } else {
+                        const int c1 = col1 > 1 ? col1 - 1 : 0;
+                        const uint32_t A = tab[d * WMAX + c1];
+                        const uint32_t Bd = tab[dm1 * WMAX + c1];
+                        const uint32_t Bu = tab[dm1 * WMAX + jq - 1];
+                        int a1 = cbase + col1, a2 = cbase + jq;
+                        a1 = a1 < 0 ? 0 : (a1 > GE::BAND_MAX ? GE::BAND_MAX : a1);
+                        a2 = a2 < 0 ? 0 : (a2 > GE::BAND_MAX ? GE::BAND_MAX : a2);
+                        mb = A >> (unsigned)(iq - 1 - a1);
+                        sb = Bd >> (unsigned)(iq - 1 - a1);
+                        db = Bd >> (unsigned)(iq - a1);
+                        ib = Bu >> (unsigned)(iq - 1 - a2);
                     }
-                    const unsigned nz = (__ballot_sync(gmask, op != OP_M) >> gbase) & lowmask;
-                    const int f = nz ? __ffs(nz) - 1 : G;
-#ifdef GA_DEBUG
-                    if (pair == 1)
-                        printf("TB q=%d state d=%d j=%d i=%d c=%d -> lane (jq=%d iq=%d) op=%d f=%d\n", q,
-                               d, j, i, consumed, jq, iq, op, f);
-#endif
-                    if (q < f) ops[nops + q] = '=';
-                    wreads += __reduce_add_sync(gmask, q < f ? (unsigned)rd : 0u);
+                    if (jq == 1) {  // column 0 is init(m, .): bit x inactive iff x >= level
+                        mb = iq - 1 >= d;
+                        sb = iq - 1 >= d - 1;
+                        db = iq >= d - 1;
+                    }
+                    const bool mok = symeq && (iq == 0 || !(mb & 1u));
+                    const bool dpos = d > 0;
+                    const bool sok = dpos && (iq == 0 || !(sb & 1u));
+                    const bool iok = dpos && (iq == 0 || !(ib & 1u));
+                    const bool dok = dpos && !(db & 1u);
+                    const unsigned okm = (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 |
+                                         (unsigned)dok << 3;
+                    op = (int)((P.prio_lut >> (4 * okm)) & 0xFu);
+                    rd = (unsigned)(jq >= 2) + (dpos ? (unsigned)(jq >= 2) + 1u : 0u);
+                }
+                const unsigned nz = (__ballot_sync(FULL, op != OP_M) >> gbase) & lowmask;
+                const int f = nz ? __ffs(nz) - 1 : G;
+                const int opf = __shfl_sync(FULL, op, f & (G - 1), G);
+                if (going) {
+                    if (q < f) {
+                        ops[nops + q] = '=';
+                        lreads += rd;
+                    }
                     j -= f;
                     i -= f;
                     consumed += f;
                     tcons += f;
                     nops += f;
-                    if (f == G) continue;
-                    const int opf = __shfl_sync(gmask, op, f, G);
-                    const int rdf = __shfl_sync(gmask, rd, f, G);
-                    if (opf == OP_STOP) continue;
-                    if (opf == OP_STUCK) {
-                        stuck = true;
-                        break;
+                    if (f < G && opf != OP_STOP) {
+                        if (opf == OP_STUCK) {
+                            stuck = true;
+                            going = false;
+                        } else {
+                            if (q == f) lreads += rd;
+                            uint8_t ch;
+                            if (opf == OP_S) {
+                                ch = 'X'; --j; --d; --i; ++consumed; ++tcons;
+                            } else if (opf == OP_I) {
+                                ch = 'I'; --d; --i; ++consumed;
+                            } else {
+                                ch = 'D'; --j; --d; ++tcons;
+                            }
+                            if (q == 0) ops[nops] = ch;
+                            ++nops;
+                            ++wcost;
+                        }
                     }
-                    wreads += rdf;
-                    uint8_t ch;
-                    if (opf == OP_S) {
-                        ch = 'X'; --j; --d; --i; ++consumed; ++tcons;
-                    } else if (opf == OP_I) {
-                        ch = 'I'; --d; --i; ++consumed;
-                    } else {
-                        ch = 'D'; --j; --d; ++tcons;
-                    }
-                    ++wcost;
-                    if (q == 0) ops[nops] = ch;
-                    ++nops;
                 }
-                // entry_writes / words_allocated of this window in closed form
-                // (sum over stored columns per level, dptable.py:62-82, 156-171)
-                unsigned wr = 0;
+            }
+            // entry_writes / words_allocated of this window in closed form
+            // (stored columns per level, dptable.py:62-82, 156-171)
+            unsigned wr = 0;
+            if (tbg && !stuck) {
                 for (int dd = q; dd <= d_min; dd += G) {
                     int ss = n - budget - (K - dd) - 1;
                     ss = ss > 1 ? ss : 1;
                     const int cnt = n - ss + 1;
                     wr += cnt > 0 ? (unsigned)cnt : 0u;
                 }
-                wr = __reduce_add_sync(gmask, wr);
+            }
+            wr = group_sum<G>(wr);
+            lreads = group_sum<G>(lreads);
+            if (tbg) {
                 if (stuck) {
                     write_result(3, widx);
                     phase = NEED_PAIR;
@@ -467,7 +502,7 @@ genasm_kernel(const KernelParams P) {
                         dists[widx] = (uint8_t)d_min;
                         rows += d_min + 1;
                         cost += wcost;
-                        reads += wreads;
+                        reads += lreads;
                         writes += wr;
                         words += (int64_t)wr * ((m + 63) / 64);
                     }

@@ -53,6 +53,7 @@ struct KernelParams {
     int64_t n_pairs;
     int32_t W, O, k;
     uint32_t prio;             // 4 x 2-bit edge ids, first choice in bits 0-1 (0=M 1=S 2=I 3=D)
+    uint64_t prio_lut;         // active-edge mask (M|S<<1|I<<2|D<<3) -> chosen edge, 4 bits each
     void* results;             // ga_pair_result[n_pairs]
     const int64_t* ops_off;
     uint8_t* ops;
