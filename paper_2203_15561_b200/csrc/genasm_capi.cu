@@ -225,10 +225,16 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     P.queue = c->queue;
     e = cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
-    const int group = env_int("GA_GROUP", 16);
-    const int block = env_int("GA_BLOCK", 64);
-    e = genasm::launch_genasm(P, group, block, c->num_sms, st, &c->overflow, &c->overflow_cap,
-                              &c->last_shape);
+    const char* kind = getenv("GA_KERNEL");
+    if (kind && strcmp(kind, "lockstep") == 0) {
+        const int group = env_int("GA_GROUP", 16);
+        const int block = env_int("GA_BLOCK", 64);
+        e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &c->overflow,
+                                           &c->overflow_cap, &c->last_shape);
+    } else {
+        e = genasm::launch_genasm_ws(P, env_int("GA_DC_WARPS", 0), c->num_sms, st, &c->overflow,
+                                     &c->overflow_cap, &c->last_shape);
+    }
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     c->launches = 1;
     return 0;

@@ -74,8 +74,14 @@ struct LaunchShape {
     int64_t overflow_words_per_group;
 };
 
-cudaError_t launch_genasm(const KernelParams& P, int group, int block_threads, int num_sms,
-                          cudaStream_t stream, uint32_t** overflow, size_t* cap,
-                          LaunchShape* shape);
+// lock-step kernel (genasm_lockstep.cu): every group does DC, TB and setup
+cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_threads,
+                                   int num_sms, cudaStream_t stream, uint32_t** overflow,
+                                   size_t* cap, LaunchShape* shape);
+
+// warp-specialised kernel (genasm_ws.cu): DC warps + traceback warps per CTA
+cudaError_t launch_genasm_ws(const KernelParams& P, int dc_warps, int num_sms,
+                             cudaStream_t stream, uint32_t** overflow, size_t* cap,
+                             LaunchShape* shape);
 
 }  // namespace genasm

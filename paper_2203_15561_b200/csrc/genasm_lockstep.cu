@@ -1,182 +1,11 @@
-// genasm_kernel.cu -- fused windowed GenASM-DC + GenASM-TB kernel (sm_100a).
-// Design summary in genasm_kernel.cuh; roofline and layout in DESIGN.md.
-#include <cuda_runtime.h>
-#include <stdint.h>
-#include <stdio.h>
-
-#include "genasm_kernel.cuh"
+// genasm_lockstep.cu -- lock-step variant of the fused DC+TB kernel (sm_100a):
+// every group of G lanes owns one pair and runs DC, traceback and window
+// setup itself; the groups of a warp advance in pass rounds.  Kept as the
+// fallback/comparison path (GA_KERNEL=lockstep); the default is the
+// warp-specialised kernel in genasm_ws.cu.
+#include "genasm_device.cuh"
 
 namespace genasm {
-
-constexpr int kMaxBlock = 256;
-
-enum : int { NEED_PAIR = 0, NEED_WINDOW = 1, IN_DC = 2, IN_TB = 3, DONE = 4 };
-enum : int { OP_M = 0, OP_S = 1, OP_I = 2, OP_D = 3, OP_STOP = 4, OP_STUCK = 5 };
-
-// ---- bit rows: NW little-endian 32-bit words, 0 = active ----
-
-// init(m, d): bits < min(d, m) are 0 (bitvec.py:108-122); bits >= m are
-// don't-care and left 1.
-template <int NW>
-__device__ __forceinline__ void init_row(uint32_t (&r)[NW], int m, int d) {
-    const int z = d < m ? d : m;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const int lo = 32 * w;
-        uint32_t zero;
-        if (z >= lo + 32) zero = 0xffffffffu;
-        else if (z <= lo) zero = 0u;
-        else zero = (1u << (z - lo)) - 1u;
-        r[w] = ~zero;
-    }
-}
-
-// shift toward higher bit index by one, shifting in an active 0 (bitvec.py:68-74)
-template <int NW>
-__device__ __forceinline__ void shl1(const uint32_t (&x)[NW], uint32_t (&r)[NW]) {
-    r[0] = x[0] << 1;
-#pragma unroll
-    for (int w = 1; w < NW; ++w) r[w] = __funnelshift_l(x[w - 1], x[w], 1);
-}
-
-template <int NW>
-__device__ __forceinline__ uint32_t word_sel(const uint32_t (&x)[NW], int w) {
-    uint32_t v = x[0];
-#pragma unroll
-    for (int u = 1; u < NW; ++u) v = (w == u) ? x[u] : v;
-    return v;
-}
-
-// 32-bit band of a row starting at bit `amt` (0 <= amt <= 32*NW-32)
-template <int NW>
-__device__ __forceinline__ uint32_t band32(const uint32_t (&r)[NW], int amt) {
-    if (NW == 1) return r[0];
-    if (NW == 2) return __funnelshift_rc(r[0], r[NW - 1], (unsigned)amt);
-    const int wi = amt >> 5;
-    const int wj = wi + 1 < NW ? wi + 1 : NW - 1;
-    return __funnelshift_r(word_sel<NW>(r, wi), word_sel<NW>(r, wj), (unsigned)(amt & 31));
-}
-
-template <int NW>
-struct Geo {
-    static constexpr int WMAX = 32 * NW;
-    static constexpr bool BAND = NW >= 2;     // 32-bit band entries (else full 32-bit rows)
-    static constexpr int LV = BAND ? 16 : 40;  // table levels resident in shared memory
-    static constexpr int TAB_W = LV * WMAX;    // words
-    static constexpr int GROUP_W = TAB_W + 2 * WMAX * NW + WMAX / 2;
-    static constexpr int BAND_MAX = 32 * NW - 32;
-};
-
-// One lane of the DC wavefront: level d = pass*G + q; at step s it evaluates
-// column j = s-q+1 of R[d] (distance.py:125-149), receiving R[d-1][j] from
-// lane q-1 by shuffle (lane 0: the carry row of the previous pass).
-// PRED: fill/drain steps where some lanes are outside [1, n]; MIXED: some
-// group of the warp stores full-width rows (full mode) this round.
-template <int NW, int G>
-struct DcLane {
-    using GE = Geo<NW>;
-    uint32_t v[NW], a[NW], outv[NW];
-    uint32_t lvl0;
-    int q, n, amt_base;
-    bool active, lane0carry, lastlane, full;
-    uint32_t* trow;
-    uint32_t* grow;
-    uint32_t* crow;
-    const uint32_t* prow;
-
-    __device__ __forceinline__ void init(int q_, bool in_dc, int pass, int m, int n_, int K, int W,
-                                         bool full_, uint32_t* tab, uint32_t* carry,
-                                         const uint32_t* pmcol, uint32_t* gtab) {
-        q = q_;
-        n = n_;
-        const int d = pass * G + q;
-        active = in_dc && d <= K;
-        lane0carry = active && q == 0 && d > 0;
-        lastlane = active && q == G - 1;
-        full = full_;
-        init_row<NW>(v, m, d);                // R[d][0] = init(m, d)
-        init_row<NW>(a, m, d > 0 ? d - 1 : 0);  // R[d-1][0]
-        lvl0 = d == 0 ? 0xffffffffu : 0u;     // level 0 has only the match edge
-#pragma unroll
-        for (int w = 0; w < NW; ++w) outv[w] = 0u;
-        amt_base = m - n - 15 - q;            // band origin of column j = s-q+1
-        const int dd = d < GE::LV ? d : 0;
-        trow = tab + dd * GE::WMAX;
-        grow = gtab + (int64_t)d * W * NW;
-        crow = carry;
-        prow = pmcol;
-    }
-
-    template <bool PRED, bool MIXED>
-    __device__ __forceinline__ void step(int s) {
-        uint32_t b[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
-        const int c = s - q;  // column j-1
-        const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
-        if (PRED) {
-            // branch-free fill/drain: every c in [-(G-1), n+G-2] addresses words
-            // inside this group's shared region, so the loads need no guard
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t cw = crow[c * NW + w];
-                b[w] = lane0carry ? cw : b[w];
-            }
-        } else if (lane0carry) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) b[w] = crow[c * NW + w];
-        }
-        uint32_t tt[NW], st[NW], sv[NW], r[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
-        shl1<NW>(tt, st);
-        shl1<NW>(v, sv);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t pm = prow[c * NW + w];
-            r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
-        }
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            a[w] = PRED ? (inr ? b[w] : a[w]) : b[w];
-            v[w] = PRED ? (inr ? r[w] : v[w]) : r[w];
-            outv[w] = PRED ? (inr ? r[w] : outv[w]) : r[w];
-        }
-        if (inr) {
-            if (!GE::BAND) {
-                trow[c] = r[0];
-            } else if (MIXED && full) {
-#pragma unroll
-                for (int w = 0; w < NW; ++w) grow[c * NW + w] = r[w];
-            } else {
-                int amt = amt_base + s;
-                amt = amt < 0 ? 0 : amt;
-                if (NW > 2) amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
-                trow[c] = band32<NW>(r, amt);
-            }
-        }
-        if (lastlane && inr) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) crow[c * NW + w] = r[w];
-        }
-    }
-};
-
-constexpr unsigned FULL = 0xffffffffu;
-
-// reductions over the G lanes of a group, all 32 lanes participating
-template <int G>
-__device__ __forceinline__ unsigned group_sum(unsigned x) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o, G);
-    return x;
-}
-template <int G>
-__device__ __forceinline__ unsigned group_or(unsigned x) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) x |= __shfl_xor_sync(FULL, x, o, G);
-    return x;
-}
 
 template <int NW, int G>
 __global__ void __launch_bounds__(kMaxBlock)
@@ -574,7 +403,7 @@ static cudaError_t launch_nw(const KernelParams& P, int group, int block, int nu
     }
 }
 
-cudaError_t launch_genasm(const KernelParams& P, int group, int block, int num_sms,
+cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block, int num_sms,
                           cudaStream_t stream, uint32_t** overflow, size_t* cap,
                           LaunchShape* shape) {
     if (P.W <= 32) return launch_nw<1>(P, group, block, num_sms, stream, overflow, cap, shape);
