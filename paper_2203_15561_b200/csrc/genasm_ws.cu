@@ -44,6 +44,98 @@ struct WsGeo {
     static constexpr int CARRY_W = GE::WMAX * NW;
 };
 
+struct TbWalk {
+    int d, j, i, consumed, tcons, wcost, no;
+    unsigned lreads;
+    bool stuck;
+};
+
+// The traceback walk of one window by one lane, up to column 0 (the caller
+// applies the column-0 insertion rule).  Per state (d, j, i): edge bits from
+// three table words (backtrace.py:84-99), first active edge by the priority
+// LUT, then a branch-free state update.  FULLMODE reads full-width rows from
+// the slot's global slab, otherwise the 32-bit band (or W <= 32 rows) in smem.
+template <int NW, bool FULLMODE>
+__device__ __forceinline__ void tb_walk(TbWalk& w, const uint32_t* __restrict__ tab,
+                                        const uint32_t* __restrict__ gt,
+                                        const uint8_t* __restrict__ cp,
+                                        const uint8_t* __restrict__ ct, int m, int n, int W,
+                                        int budget, uint64_t lut, uint8_t* __restrict__ out) {
+    using GE = Geo<NW>;
+    constexpr int WMAX = GE::WMAX;
+    const int cbase = m - 1 - n - 15;  // band origin of column col: clamp(cbase + col)
+    int d = w.d, j = w.j, i = w.i, consumed = w.consumed, tcons = w.tcons, wcost = w.wcost;
+    int no = w.no;
+    unsigned lreads = w.lreads;
+    while (i >= 0 && consumed < budget && j > 0) {
+        const int col1 = j - 1;
+        const int dm1 = d > 0 ? d - 1 : 0;
+        const int tcode = ct[col1];
+        const int pcode = cp[i];
+        uint32_t mb, sb, db, ib;  // table bits, 1 = inactive
+        if (FULLMODE) {
+            const int c = col1 > 1 ? col1 - 1 : 0;
+            const int x0 = i > 0 ? i - 1 : 0;
+            const uint32_t* rA = gt + ((int64_t)d * W + c) * NW;
+            const uint32_t* rB = gt + ((int64_t)dm1 * W + c) * NW;
+            const uint32_t* rU = gt + ((int64_t)dm1 * W + col1) * NW;
+            mb = rA[x0 >> 5] >> (x0 & 31);
+            sb = rB[x0 >> 5] >> (x0 & 31);
+            db = rB[i >> 5] >> (i & 31);
+            ib = rU[x0 >> 5] >> (x0 & 31);
+        } else {
+            const int c = col1 > 1 ? col1 - 1 : 0;
+            const uint32_t A = tab[d * WMAX + c];
+            const uint32_t Bd = tab[dm1 * WMAX + c];
+            const uint32_t Bu = tab[dm1 * WMAX + col1];
+            int a1 = cbase + col1;
+            a1 = a1 < 0 ? 0 : (a1 > GE::BAND_MAX ? GE::BAND_MAX : a1);
+            int a2 = cbase + j;
+            a2 = a2 < 0 ? 0 : (a2 > GE::BAND_MAX ? GE::BAND_MAX : a2);
+            mb = A >> (unsigned)(i - 1 - a1);
+            sb = Bd >> (unsigned)(i - 1 - a1);
+            db = Bd >> (unsigned)(i - a1);
+            ib = Bu >> (unsigned)(i - 1 - a2);
+        }
+        if (col1 == 0) {  // column 0 is init(m, .): bit x inactive iff x >= level
+            mb = i - 1 >= d;
+            sb = i - 1 >= d - 1;
+            db = i >= d - 1;
+        }
+        const unsigned dpos = d > 0;
+        const unsigned i0 = i == 0;
+        const unsigned mok = (unsigned)(tcode < 4) & (unsigned)(pcode == tcode) & (i0 | (~mb & 1u));
+        const unsigned sok = dpos & (i0 | (~sb & 1u));
+        const unsigned iok = dpos & (i0 | (~ib & 1u));
+        const unsigned dok = dpos & (~db & 1u);
+        const unsigned okm = mok | sok << 1 | iok << 2 | dok << 3;
+        const unsigned op = (unsigned)(lut >> (4 * okm)) & 0xFu;
+        if (op > OP_D) {
+            w.stuck = true;
+            break;
+        }
+        const unsigned j2 = j >= 2;
+        lreads += j2 + (dpos ? j2 + 1u : 0u);
+        // op in M,S,I,D = 0..3: j moves on M,S,D; d on S,I,D; i (and consumed) on M,S,I
+        const int dj = (0xBu >> op) & 1u, dd = (0xEu >> op) & 1u, di = (0x7u >> op) & 1u;
+        out[no++] = (uint8_t)(0x4449583Du >> (8 * op));  // "=XID"
+        j -= dj;
+        d -= dd;
+        i -= di;
+        consumed += di;
+        tcons += dj;
+        wcost += dd;
+    }
+    w.d = d;
+    w.j = j;
+    w.i = i;
+    w.consumed = consumed;
+    w.tcons = tcons;
+    w.wcost = wcost;
+    w.no = no;
+    w.lreads = lreads;
+}
+
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
 
@@ -290,90 +382,40 @@ genasm_ws_kernel(const KernelParams P, const int nd) {
                     st = S_EMPTY;
                 } else {
                     // ---- scalar traceback (backtrace.py:113-160) ----
-                    const bool full = BAND && M.full;
-                    int d = d_min, j = n, i = m - 1, consumed = 0, tcons = 0, wcost = 0;
-                    unsigned lreads = 0;
-                    bool stuck = false;
-                    const int cbase = m - 1 - n - 15;  // band origin of column col: cbase + col
+                    TbWalk w;
+                    w.d = d_min;
+                    w.j = n;
+                    w.i = m - 1;
+                    w.consumed = w.tcons = w.wcost = w.no = 0;
+                    w.lreads = 0;
+                    w.stuck = false;
                     uint8_t* out = ops + nops;
-                    int no = 0;
-                    for (;;) {
-                        if (i < 0 || consumed >= budget) break;
-                        if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
-                            if (i + 1 > d) {
-                                stuck = true;
-                                break;
-                            }
-                            const int take = (i + 1 < budget - consumed) ? i + 1 : budget - consumed;
-                            for (int u = 0; u < take; ++u) out[no + u] = 'I';
-                            no += take;
-                            wcost += take;
-                            consumed += take;
-                            i -= take;
-                            break;
-                        }
-                        const int tcode = ct[j - 1];
-                        const bool symeq = tcode < 4 && cp[i] == tcode;
-                        const int dm1 = d > 0 ? d - 1 : 0;
-                        const int col1 = j - 1;
-                        uint32_t mb, sb, db, ib;  // table bits, 1 = inactive
-                        if (full) {
-                            auto gbit = [&](int e, int col, int x) -> uint32_t {
-                                col = col > 1 ? col : 1;
-                                x = x > 0 ? x : 0;
-                                const uint32_t* row = gt + ((int64_t)e * W + (col - 1)) * NW;
-                                return row[x >> 5] >> (x & 31);
-                            };
-                            mb = gbit(d, col1, i - 1);
-                            sb = gbit(dm1, col1, i - 1);
-                            db = gbit(dm1, col1, i);
-                            ib = gbit(dm1, j, i - 1);
-                        } else {
-                            const int c1 = col1 > 1 ? col1 - 1 : 0;
-                            const uint32_t A = tab[d * WMAX + c1];
-                            const uint32_t Bd = tab[dm1 * WMAX + c1];
-                            const uint32_t Bu = tab[dm1 * WMAX + j - 1];
-                            int a1 = cbase + col1, a2 = cbase + j;
-                            a1 = a1 < 0 ? 0 : (a1 > GE::BAND_MAX ? GE::BAND_MAX : a1);
-                            a2 = a2 < 0 ? 0 : (a2 > GE::BAND_MAX ? GE::BAND_MAX : a2);
-                            mb = A >> (unsigned)(i - 1 - a1);
-                            sb = Bd >> (unsigned)(i - 1 - a1);
-                            db = Bd >> (unsigned)(i - a1);
-                            ib = Bu >> (unsigned)(i - 1 - a2);
-                        }
-                        if (j == 1) {  // column 0 is init(m, .): bit x inactive iff x >= level
-                            mb = i - 1 >= d;
-                            sb = i - 1 >= d - 1;
-                            db = i >= d - 1;
-                        }
-                        const bool dpos = d > 0;
-                        const bool mok = symeq && (i == 0 || !(mb & 1u));
-                        const bool sok = dpos && (i == 0 || !(sb & 1u));
-                        const bool iok = dpos && (i == 0 || !(ib & 1u));
-                        const bool dok = dpos && !(db & 1u);
-                        const unsigned okm = (unsigned)mok | (unsigned)sok << 1 |
-                                             (unsigned)iok << 2 | (unsigned)dok << 3;
-                        const int op = (int)((P.prio_lut >> (4 * okm)) & 0xFu);
-                        if (op > OP_D) {
-                            stuck = true;
-                            break;
-                        }
-                        lreads += (unsigned)(j >= 2) + (dpos ? (unsigned)(j >= 2) + 1u : 0u);
-                        uint8_t ch;
-                        if (op == OP_M) {
-                            ch = '='; --j; --i; ++consumed; ++tcons;
-                        } else if (op == OP_S) {
-                            ch = 'X'; --j; --d; --i; ++consumed; ++tcons; ++wcost;
-                        } else if (op == OP_I) {
-                            ch = 'I'; --d; --i; ++consumed; ++wcost;
-                        } else {
-                            ch = 'D'; --j; --d; ++tcons; ++wcost;
-                        }
-                        out[no++] = ch;
+                    if (BAND && M.full) {
+                        tb_walk<NW, true>(w, tab, gt, cp, ct, m, n, W, budget, P.prio_lut, out);
+                    } else {
+                        tb_walk<NW, false>(w, tab, gt, cp, ct, m, n, W, budget, P.prio_lut, out);
                     }
+                    // column 0 (reached with pattern and budget left): the init zeros
+                    // cover i+1 insertions at level d (backtrace.py:122-132)
+                    if (!w.stuck && w.i >= 0 && w.consumed < budget && w.j == 0) {
+                        if (w.i + 1 > w.d) {
+                            w.stuck = true;
+                        } else {
+                            const int left = budget - w.consumed;
+                            const int take = w.i + 1 < left ? w.i + 1 : left;
+                            for (int u = 0; u < take; ++u) out[w.no + u] = 'I';
+                            w.no += take;
+                            w.wcost += take;
+                            w.consumed += take;
+                            w.i -= take;
+                        }
+                    }
+                    const bool stuck = w.stuck;
+                    const int consumed = w.consumed, tcons = w.tcons, wcost = w.wcost, no = w.no;
+                    const unsigned lreads = w.lreads;
 #ifdef GA_DEBUG
                     printf("TB slot %d widx=%d d_min=%d full=%d m=%d n=%d consumed=%d tcons=%d stuck=%d\n",
-                           s, widx, d_min, (int)full, m, n, consumed, tcons, (int)stuck);
+                           s, widx, d_min, M.full, m, n, consumed, tcons, (int)stuck);
 #endif
                     if (stuck) {
                         finish(3, widx);
