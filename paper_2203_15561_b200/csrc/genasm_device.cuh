@@ -72,12 +72,18 @@ struct Geo {
 // One lane of the DC wavefront: level d = pass*G + q; at step s it evaluates
 // column j = s-q+1 of R[d] (distance.py:125-149), receiving R[d-1][j] from
 // lane q-1 by shuffle (lane 0: the carry row of the previous pass).
+// The recurrence is regrouped as
+//     R[d][j] = ((sh(v) | pm) & (sh(a) & a)) & sh(b)
+// (a = R[d-1][j-1], b = R[d-1][j], v = R[d][j-1]; sh(a&b) = sh(a)&sh(b)), so
+// only sh(b) and one LOP3 sit between the shuffle of step s and the shuffle of
+// step s+1; sh(a) is sh(b) of the previous step.  The per-column mask and the
+// carry word are loaded one step ahead.
 // PRED: fill/drain steps where some lanes are outside [1, n]; MIXED: some
 // group of the warp stores full-width rows (full mode) this round.
 template <int NW, int G>
 struct DcLane {
     using GE = Geo<NW>;
-    uint32_t v[NW], a[NW], outv[NW];
+    uint32_t v[NW], a[NW], sha[NW], outv[NW], npm[NW], ncw[NW];
     uint32_t lvl0;
     int q, n, amt_base;
     bool active, lane0carry, lastlane, full;
@@ -96,51 +102,54 @@ struct DcLane {
         lane0carry = active && q == 0 && d > 0;
         lastlane = active && q == G - 1;
         full = full_;
-        init_row<NW>(v, m, d);                // R[d][0] = init(m, d)
+        init_row<NW>(v, m, d);                  // R[d][0] = init(m, d)
         init_row<NW>(a, m, d > 0 ? d - 1 : 0);  // R[d-1][0]
-        lvl0 = d == 0 ? 0xffffffffu : 0u;     // level 0 has only the match edge
+        shl1<NW>(a, sha);
+        lvl0 = d == 0 ? 0xffffffffu : 0u;       // level 0 has only the match edge
 #pragma unroll
         for (int w = 0; w < NW; ++w) outv[w] = 0u;
-        amt_base = m - n - 15 - q;            // band origin of column j = s-q+1
+        amt_base = m - n - 15 - q;              // band origin of column j = s-q+1
         const int dd = d < GE::LV ? d : 0;
         trow = tab + dd * GE::WMAX;
         grow = gtab + (int64_t)d * W * NW;
         crow = carry;
         prow = pmcol;
+        // column index c = s - q of step 0; every c in [-(G-1), n+G-1] addresses
+        // words inside this group's shared region, so the loads need no guard
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            npm[w] = prow[-q * NW + w];
+            ncw[w] = crow[-q * NW + w];
+        }
     }
 
     template <bool PRED, bool MIXED>
     __device__ __forceinline__ void step(int s) {
-        uint32_t b[NW];
+        uint32_t b[NW], pm[NW];
 #pragma unroll
         for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
         const int c = s - q;  // column j-1
         const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
-        if (PRED) {
-            // branch-free fill/drain: every c in [-(G-1), n+G-2] addresses words
-            // inside this group's shared region, so the loads need no guard
 #pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t cw = crow[c * NW + w];
-                b[w] = lane0carry ? cw : b[w];
-            }
-        } else if (lane0carry) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) b[w] = crow[c * NW + w];
+        for (int w = 0; w < NW; ++w) {
+            b[w] = lane0carry ? ncw[w] : b[w];
+            pm[w] = npm[w];
+            npm[w] = prow[(c + 1) * NW + w];  // prefetch the next step's words
+            ncw[w] = crow[(c + 1) * NW + w];
         }
-        uint32_t tt[NW], st[NW], sv[NW], r[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) tt[w] = a[w] & b[w];
-        shl1<NW>(tt, st);
+        uint32_t shb[NW], sv[NW], r[NW];
+        shl1<NW>(b, shb);
         shl1<NW>(v, sv);
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const uint32_t pm = prow[c * NW + w];
-            r[w] = (sv[w] | pm) & ((st[w] & a[w]) | lvl0);
+            const uint32_t x = (sha[w] & a[w]) | lvl0;     // S and D edges (off the chain)
+            const uint32_t t = (sv[w] | pm[w]) & x;        // M edge (off the chain)
+            r[w] = t & (shb[w] | lvl0);                    // I edge
         }
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             a[w] = PRED ? (inr ? b[w] : a[w]) : b[w];
+            sha[w] = PRED ? (inr ? shb[w] : sha[w]) : shb[w];
             v[w] = PRED ? (inr ? r[w] : v[w]) : r[w];
             outv[w] = PRED ? (inr ? r[w] : outv[w]) : r[w];
         }
