@@ -79,7 +79,11 @@ cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_t
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,
                                    size_t* cap, LaunchShape* shape);
 
-// warp-specialised kernel (genasm_ws.cu): DC warps + traceback warps per CTA
+// thread-per-window column-major kernel (genasm_colmajor.cu)
+cudaError_t launch_genasm_colmajor(const KernelParams& P, int num_sms, cudaStream_t stream,
+                                   uint32_t** overflow, size_t* cap, LaunchShape* shape);
+
+// warp-specialised kernel (genasm_pipeline.cu): DC warps + traceback warps per CTA
 cudaError_t launch_genasm_ws(const KernelParams& P, int dc_warps, int num_sms,
                              cudaStream_t stream, uint32_t** overflow, size_t* cap,
                              LaunchShape* shape);
