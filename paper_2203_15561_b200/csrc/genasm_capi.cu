@@ -230,8 +230,8 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
         e = genasm::launch_genasm_colmajor(P, c->num_sms, st, &c->overflow, &c->overflow_cap,
                                            &c->last_shape);
     } else if (kind && strcmp(kind, "lockstep") == 0) {
-        const int group = env_int("GA_GROUP", 16);
-        const int block = env_int("GA_BLOCK", 64);
+        const int group = env_int("GA_GROUP", 4);
+        const int block = env_int("GA_BLOCK", 0);
         e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &c->overflow,
                                            &c->overflow_cap, &c->last_shape);
     } else {

@@ -189,5 +189,142 @@ __device__ __forceinline__ unsigned group_or(unsigned x) {
     return x;
 }
 
+// One lane of a multi-level DC wavefront: a group of G lanes covers G*LPL
+// consecutive levels per pass; lane q owns levels dq .. dq+LPL-1 with
+// dq = pass*G*LPL + q*LPL and at step s evaluates column j = s-q+1 of all of
+// them, column-major inside the lane (distance.py:125-149):
+//   R[d][j] = (sh(R[d][j-1]) | PM[T[j-1]]) & sh(R[d-1][j-1] & R[d-1][j]) & R[d-1][j-1]
+// Level dq takes R[dq-1][j] from lane q-1 by one shuffle (lane 0: the carry
+// row of the previous pass); levels dq+1.. use the lane's own registers.  One
+// shuffle, one mask load and a few address updates are shared by LPL entries.
+// PRED: fill/drain steps where some lanes are outside [1, n]; MIXED: some
+// group of the warp stores full-width rows (full mode) this round.
+template <int NW, int G, int LPL>
+struct DcLaneM {
+    using GE = Geo<NW>;
+    uint32_t col[LPL][NW], a0[NW], outv[NW], npm[NW], ncw[NW];
+    uint32_t lvl0;
+    int q, n, dq, K, amt_base;
+    bool active, lane0carry, lastlane, full;
+    uint32_t* trow;
+    uint32_t* grow;
+    uint32_t* crow;
+    const uint32_t* prow;
+
+    __device__ __forceinline__ void init(int q_, bool in_dc, int pass, int m, int n_, int K_, int W,
+                                         bool full_, uint32_t* tab, uint32_t* carry,
+                                         const uint32_t* pmcol, uint32_t* gtab) {
+        q = q_;
+        n = n_;
+        K = K_;
+        dq = pass * G * LPL + q * LPL;
+        active = in_dc && dq <= K;
+        lane0carry = active && q == 0 && dq > 0;
+        lastlane = active && q == G - 1;
+        full = full_;
+#pragma unroll
+        for (int k = 0; k < LPL; ++k) init_row<NW>(col[k], m, dq + k);  // R[d][0] = init(m, d)
+        init_row<NW>(a0, m, dq > 0 ? dq - 1 : 0);                          // R[dq-1][0]
+        lvl0 = dq == 0 ? 0xffffffffu : 0u;  // level 0 has only the match edge
+#pragma unroll
+        for (int w = 0; w < NW; ++w) outv[w] = 0u;
+        amt_base = m - n - 15 - q;  // band origin of column j = s-q+1
+        const int dd = dq + LPL <= GE::LV ? dq : 0;
+        trow = tab + dd * GE::WMAX;
+        grow = gtab + (int64_t)dq * W * NW;
+        gstride_ = (int64_t)W * NW;
+        crow = carry;
+        prow = pmcol;
+        // column index c = s - q of step 0; every c in [-(G-1), n+G-1] addresses
+        // words inside this group's shared region, so the loads need no guard
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            npm[w] = prow[-q * NW + w];
+            ncw[w] = crow[-q * NW + w];
+        }
+    }
+
+    template <bool PRED, bool MIXED>
+    __device__ __forceinline__ void step(int s) {
+        uint32_t b[NW], pm[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
+        const int c = s - q;  // column j-1
+        const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            b[w] = lane0carry ? ncw[w] : b[w];
+            pm[w] = npm[w];
+            npm[w] = prow[(c + 1) * NW + w];  // prefetch the next step's words
+            ncw[w] = crow[(c + 1) * NW + w];
+        }
+        uint32_t nc[LPL][NW];
+        {
+            uint32_t tt[NW], st[NW], sv[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) tt[w] = a0[w] & b[w];
+            shl1<NW>(tt, st);
+            shl1<NW>(col[0], sv);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) nc[0][w] = (sv[w] | pm[w]) & ((st[w] & a0[w]) | lvl0);
+        }
+#pragma unroll
+        for (int k = 1; k < LPL; ++k) {
+            uint32_t tt[NW], st[NW], sv[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) tt[w] = col[k - 1][w] & nc[k - 1][w];
+            shl1<NW>(tt, st);
+            shl1<NW>(col[k], sv);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) nc[k][w] = (sv[w] | pm[w]) & st[w] & col[k - 1][w];
+        }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            a0[w] = PRED ? (inr ? b[w] : a0[w]) : b[w];
+            outv[w] = PRED ? (inr ? nc[LPL - 1][w] : outv[w]) : nc[LPL - 1][w];
+        }
+#pragma unroll
+        for (int k = 0; k < LPL; ++k)
+#pragma unroll
+            for (int w = 0; w < NW; ++w) col[k][w] = PRED ? (inr ? nc[k][w] : col[k][w]) : nc[k][w];
+        if (inr) {
+            int amt = amt_base + s;
+            amt = amt < 0 ? 0 : amt;
+            if (NW > 2) amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
+#pragma unroll
+            for (int k = 0; k < LPL; ++k) {
+                if (!GE::BAND) {
+                    trow[k * GE::WMAX + c] = nc[k][0];
+                } else if (!(MIXED && full)) {
+                    trow[k * GE::WMAX + c] = band32<NW>(nc[k], amt);
+                }
+            }
+        }
+        if (MIXED && full && inr) {
+#pragma unroll
+            for (int k = 0; k < LPL; ++k)
+#pragma unroll
+                for (int w = 0; w < NW; ++w) grow[gstride_ * k + c * NW + w] = nc[k][w];
+        }
+        if (lastlane && inr) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) crow[c * NW + w] = nc[LPL - 1][w];
+        }
+    }
+
+    // lowest level of this lane whose column-n row has bit m-1 clear (or -1)
+    __device__ __forceinline__ int first_success(int m) const {
+        if (!active || n < 1) return -1;
+        const int tw = (m - 1) >> 5;
+        const uint32_t tb = 1u << ((m - 1) & 31);
+        int f = -1;
+#pragma unroll
+        for (int k = LPL - 1; k >= 0; --k)
+            if ((word_sel<NW>(col[k], tw) & tb) == 0u && dq + k <= K) f = k;
+        return f;
+    }
+
+    int64_t gstride_ = 0;  // words between consecutive levels in the full-mode slab
+};
 
 }  // namespace genasm

@@ -7,7 +7,7 @@
 
 namespace genasm {
 
-template <int NW, int G>
+template <int NW, int G, int LPL>
 __global__ void __launch_bounds__(kMaxBlock)
 genasm_kernel(const KernelParams P) {
     using GE = Geo<NW>;
@@ -163,7 +163,8 @@ genasm_kernel(const KernelParams P) {
         // ================= DC pass round (all groups in lock-step) =================
         {
             const bool in_dc = phase == IN_DC;
-            DcLane<NW, G> L;
+            constexpr int LPP = G * LPL;  // levels per pass
+            DcLaneM<NW, G, LPL> L;
             L.init(q, in_dc, pass, m, n, K, W, full, tab, carry, pmcol, gtab);
             // warp-uniform trip counts: fill [0, G-1), steady [G-1, nmin), drain [.., steps)
             const int steps = __reduce_max_sync(FULL, in_dc ? n + G - 1 : 0);
@@ -180,17 +181,18 @@ genasm_kernel(const KernelParams P) {
                 for (int s = fill_end; s < steady_end; ++s) L.template step<false, false>(s);
                 for (int s = steady_end; s < steps; ++s) L.template step<true, false>(s);
             }
-            const bool succ = L.active && n >= 1 &&
-                              (word_sel<NW>(L.v, (m - 1) >> 5) & (1u << ((m - 1) & 31))) == 0u;
-            const unsigned bal = (__ballot_sync(FULL, succ) >> gbase) & lowmask;
+            const int fs = L.first_success(m);
+            const unsigned bal = (__ballot_sync(FULL, fs >= 0) >> gbase) & lowmask;
+            const int lq = bal ? __ffs(bal) - 1 : 0;  // lowest lane holding a solved level
+            const int fsl = __shfl_sync(FULL, fs, lq, G);
             if (in_dc) {
                 if (bal) {
-                    d_min = pass * G + __ffs(bal) - 1;
+                    d_min = pass * LPP + lq * LPL + fsl;
                     phase = IN_TB;
-                } else if ((pass + 1) * G > K) {  // NotFound(k) -> WindowFailed(index, k)
+                } else if ((pass + 1) * LPP > K) {  // NotFound(k) -> WindowFailed(index, k)
                     write_result(1, widx);
                     phase = NEED_PAIR;
-                } else if (BAND && !full && (pass + 1) * G >= LV) {
+                } else if (BAND && !full && (pass + 1) * LPP >= LV) {
                     full = true;  // d_min > 15: the band cannot serve TB; redo full width
                     pass = 0;
                 } else {
@@ -352,15 +354,15 @@ genasm_kernel(const KernelParams P) {
 
 // ---------------------------------------------------------------------------
 
-template <int NW, int G>
+template <int NW, int G, int LPL>
 static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cudaStream_t stream,
                             uint32_t** overflow, size_t* overflow_cap, LaunchShape* shape) {
     using GE = Geo<NW>;
     KernelParams P = base;
-    if (block < G || block > kMaxBlock || block % 32) block = 64;
+    if (block < G || block > kMaxBlock || block % 32) block = G >= 16 ? 64 : 32;
     const int groups_per_block = block / G;
     const int smem = groups_per_block * GE::GROUP_W * 4;
-    auto kern = genasm_kernel<NW, G>;
+    auto kern = genasm_kernel<NW, G, LPL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -370,7 +372,7 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     int grid = num_sms * per_sm;
     const int64_t max_useful = (P.n_pairs + groups_per_block - 1) / groups_per_block;
     if (grid > max_useful) grid = (int)(max_useful > 0 ? max_useful : 1);
-    const int levels_cap = ((P.k + 1 + G - 1) / G) * G;
+    const int levels_cap = ((P.k + 1 + G * LPL - 1) / (G * LPL)) * (G * LPL);
     P.overflow_words_per_group = GE::BAND ? (int64_t)levels_cap * P.W * NW : 0;
     const size_t need = (size_t)grid * groups_per_block * (size_t)P.overflow_words_per_group;
     if (need > *overflow_cap || !*overflow) {
@@ -397,8 +399,10 @@ static cudaError_t launch_nw(const KernelParams& P, int group, int block, int nu
                              cudaStream_t stream, uint32_t** overflow, size_t* cap,
                              LaunchShape* shape) {
     switch (group) {
-        case 8: return launch_t<NW, 8>(P, block, num_sms, stream, overflow, cap, shape);
-        case 16: return launch_t<NW, 16>(P, block, num_sms, stream, overflow, cap, shape);
+        // G lanes x 16/G levels per lane: 16 levels per pass
+        case 4: return launch_t<NW, 4, 4>(P, block, num_sms, stream, overflow, cap, shape);
+        case 8: return launch_t<NW, 8, 2>(P, block, num_sms, stream, overflow, cap, shape);
+        case 16: return launch_t<NW, 16, 1>(P, block, num_sms, stream, overflow, cap, shape);
         default: return cudaErrorInvalidValue;
     }
 }
