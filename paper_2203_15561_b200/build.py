@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "_genasm.so")
-SOURCES = ["genasm_colmajor.cu", "genasm_pipeline.cu", "genasm_lockstep.cu", "genasm_capi.cu", "sim.cpp", "accounting.cpp",
+SOURCES = ["genasm_lockstep.cu", "genasm_capi.cu", "sim.cpp", "accounting.cpp",
            "microbench.cu"]
 HEADERS = ["genasm_kernel.cuh", "genasm_device.cuh", "../../include/genasm.h",
            "../../include/genasm_sim.h", "../../include/genasm_bench.h"]

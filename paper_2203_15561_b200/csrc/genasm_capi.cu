@@ -225,19 +225,11 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     P.queue = c->queue;
     e = cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
-    const char* kind = getenv("GA_KERNEL");
-    if (kind && strcmp(kind, "colmajor") == 0) {
-        e = genasm::launch_genasm_colmajor(P, c->num_sms, st, &c->overflow, &c->overflow_cap,
-                                           &c->last_shape);
-    } else if (kind && strcmp(kind, "lockstep") == 0) {
-        const int group = env_int("GA_GROUP", 4);
-        const int block = env_int("GA_BLOCK", 0);
-        e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &c->overflow,
-                                           &c->overflow_cap, &c->last_shape);
-    } else {
-        e = genasm::launch_genasm_ws(P, env_int("GA_DC_WARPS", 0), c->num_sms, st, &c->overflow,
-                                     &c->overflow_cap, &c->last_shape);
-    }
+    // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
+    const int group = env_int("GA_GROUP", 8);
+    const int block = env_int("GA_BLOCK", 0);
+    e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &c->overflow,
+                                       &c->overflow_cap, &c->last_shape);
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     c->launches = 1;
     return 0;

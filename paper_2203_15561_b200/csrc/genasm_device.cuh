@@ -69,110 +69,6 @@ struct Geo {
     static constexpr int BAND_MAX = 32 * NW - 32;
 };
 
-// One lane of the DC wavefront: level d = pass*G + q; at step s it evaluates
-// column j = s-q+1 of R[d] (distance.py:125-149), receiving R[d-1][j] from
-// lane q-1 by shuffle (lane 0: the carry row of the previous pass).
-// The recurrence is regrouped as
-//     R[d][j] = ((sh(v) | pm) & (sh(a) & a)) & sh(b)
-// (a = R[d-1][j-1], b = R[d-1][j], v = R[d][j-1]; sh(a&b) = sh(a)&sh(b)), so
-// only sh(b) and one LOP3 sit between the shuffle of step s and the shuffle of
-// step s+1; sh(a) is sh(b) of the previous step.  The per-column mask and the
-// carry word are loaded one step ahead.
-// PRED: fill/drain steps where some lanes are outside [1, n]; MIXED: some
-// group of the warp stores full-width rows (full mode) this round.
-template <int NW, int G>
-struct DcLane {
-    using GE = Geo<NW>;
-    uint32_t v[NW], a[NW], sha[NW], outv[NW], npm[NW], ncw[NW];
-    uint32_t lvl0;
-    int q, n, amt_base;
-    bool active, lane0carry, lastlane, full;
-    uint32_t* trow;
-    uint32_t* grow;
-    uint32_t* crow;
-    const uint32_t* prow;
-
-    __device__ __forceinline__ void init(int q_, bool in_dc, int pass, int m, int n_, int K, int W,
-                                         bool full_, uint32_t* tab, uint32_t* carry,
-                                         const uint32_t* pmcol, uint32_t* gtab) {
-        q = q_;
-        n = n_;
-        const int d = pass * G + q;
-        active = in_dc && d <= K;
-        lane0carry = active && q == 0 && d > 0;
-        lastlane = active && q == G - 1;
-        full = full_;
-        init_row<NW>(v, m, d);                  // R[d][0] = init(m, d)
-        init_row<NW>(a, m, d > 0 ? d - 1 : 0);  // R[d-1][0]
-        shl1<NW>(a, sha);
-        lvl0 = d == 0 ? 0xffffffffu : 0u;       // level 0 has only the match edge
-#pragma unroll
-        for (int w = 0; w < NW; ++w) outv[w] = 0u;
-        amt_base = m - n - 15 - q;              // band origin of column j = s-q+1
-        const int dd = d < GE::LV ? d : 0;
-        trow = tab + dd * GE::WMAX;
-        grow = gtab + (int64_t)d * W * NW;
-        crow = carry;
-        prow = pmcol;
-        // column index c = s - q of step 0; every c in [-(G-1), n+G-1] addresses
-        // words inside this group's shared region, so the loads need no guard
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            npm[w] = prow[-q * NW + w];
-            ncw[w] = crow[-q * NW + w];
-        }
-    }
-
-    template <bool PRED, bool MIXED>
-    __device__ __forceinline__ void step(int s) {
-        uint32_t b[NW], pm[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) b[w] = __shfl_up_sync(0xffffffffu, outv[w], 1, G);
-        const int c = s - q;  // column j-1
-        const bool inr = PRED ? (active && (unsigned)c < (unsigned)n) : active;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            b[w] = lane0carry ? ncw[w] : b[w];
-            pm[w] = npm[w];
-            npm[w] = prow[(c + 1) * NW + w];  // prefetch the next step's words
-            ncw[w] = crow[(c + 1) * NW + w];
-        }
-        uint32_t shb[NW], sv[NW], r[NW];
-        shl1<NW>(b, shb);
-        shl1<NW>(v, sv);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t x = (sha[w] & a[w]) | lvl0;     // S and D edges (off the chain)
-            const uint32_t t = (sv[w] | pm[w]) & x;        // M edge (off the chain)
-            r[w] = t & (shb[w] | lvl0);                    // I edge
-        }
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            a[w] = PRED ? (inr ? b[w] : a[w]) : b[w];
-            sha[w] = PRED ? (inr ? shb[w] : sha[w]) : shb[w];
-            v[w] = PRED ? (inr ? r[w] : v[w]) : r[w];
-            outv[w] = PRED ? (inr ? r[w] : outv[w]) : r[w];
-        }
-        if (inr) {
-            if (!GE::BAND) {
-                trow[c] = r[0];
-            } else if (MIXED && full) {
-#pragma unroll
-                for (int w = 0; w < NW; ++w) grow[c * NW + w] = r[w];
-            } else {
-                int amt = amt_base + s;
-                amt = amt < 0 ? 0 : amt;
-                if (NW > 2) amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
-                trow[c] = band32<NW>(r, amt);
-            }
-        }
-        if (lastlane && inr) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) crow[c * NW + w] = r[w];
-        }
-    }
-};
-
 constexpr unsigned FULL = 0xffffffffu;
 
 // reductions over the G lanes of a group, all 32 lanes participating
@@ -206,18 +102,23 @@ struct DcLaneM {
     uint32_t lvl0;
     int q, n, dq, K, amt_base;
     bool active, lane0carry, lastlane, full;
-    uint32_t* trow;
+    uint32_t* bptr;
     uint32_t* grow;
     uint32_t* crow;
     const uint32_t* prow;
 
+    // the band table lives in global memory, one region per warp, laid out
+    // [pass][step][lane][LPL]: at each step the 32 lanes store 32*LPL
+    // consecutive words (entry (d, c) of lane q was written at step c + q)
+    static constexpr int SMAX = GE::WMAX + G - 1;  // steps per pass
     __device__ __forceinline__ void init(int q_, bool in_dc, int pass, int m, int n_, int K_, int W,
-                                         bool full_, uint32_t* tab, uint32_t* carry,
+                                         bool full_, uint32_t* gband, int lane, uint32_t* carry,
                                          const uint32_t* pmcol, uint32_t* gtab) {
         q = q_;
         n = n_;
         K = K_;
         dq = pass * G * LPL + q * LPL;
+        bptr = gband + ((int64_t)pass * SMAX * 32 + lane) * LPL;
         active = in_dc && dq <= K;
         lane0carry = active && q == 0 && dq > 0;
         lastlane = active && q == G - 1;
@@ -229,8 +130,6 @@ struct DcLaneM {
 #pragma unroll
         for (int w = 0; w < NW; ++w) outv[w] = 0u;
         amt_base = m - n - 15 - q;  // band origin of column j = s-q+1
-        const int dd = dq + LPL <= GE::LV ? dq : 0;
-        trow = tab + dd * GE::WMAX;
         grow = gtab + (int64_t)dq * W * NW;
         gstride_ = (int64_t)W * NW;
         crow = carry;
@@ -287,17 +186,22 @@ struct DcLaneM {
         for (int k = 0; k < LPL; ++k)
 #pragma unroll
             for (int w = 0; w < NW; ++w) col[k][w] = PRED ? (inr ? nc[k][w] : col[k][w]) : nc[k][w];
-        if (inr) {
+        if (inr && !(MIXED && full)) {
             int amt = amt_base + s;
             amt = amt < 0 ? 0 : amt;
             if (NW > 2) amt = amt > GE::BAND_MAX ? GE::BAND_MAX : amt;
+            uint32_t bw[LPL];
 #pragma unroll
-            for (int k = 0; k < LPL; ++k) {
-                if (!GE::BAND) {
-                    trow[k * GE::WMAX + c] = nc[k][0];
-                } else if (!(MIXED && full)) {
-                    trow[k * GE::WMAX + c] = band32<NW>(nc[k], amt);
-                }
+            for (int k = 0; k < LPL; ++k) bw[k] = GE::BAND ? band32<NW>(nc[k], amt) : nc[k][0];
+            uint32_t* dst = bptr + (int64_t)s * 32 * LPL;
+            if (LPL == 4) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(bw[0], bw[LPL > 1 ? 1 : 0],
+                                                            bw[LPL > 2 ? 2 : 0], bw[LPL > 3 ? 3 : 0]);
+            } else if (LPL == 2) {
+                *reinterpret_cast<uint2*>(dst) = make_uint2(bw[0], bw[LPL > 1 ? 1 : 0]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < LPL; ++k) dst[k] = bw[k];
             }
         }
         if (MIXED && full && inr) {

@@ -9,31 +9,33 @@
 // solved in that pass then trace back together, set up their next window (or
 // pull the next pair) and rejoin at the next round.
 //
-//   DC pass (pkg/src/bitalign/distance.py:97-150): levels-as-lanes wavefront.
-//     Pass p evaluates levels pG..pG+G-1; lane q owns level d = pG+q and at
-//     step s computes column j = s-q+1, receiving R[d-1][j] from lane q-1 by
-//     one warp shuffle.  Lane 0 reads level pG-1 from the group's carry row
-//     (full-width rows of the previous pass's last level).  Rows are NW x 32-bit
-//     registers (W <= 32 NW).  Early termination (key idea 2): the window ends
-//     at the first pass holding a level whose column-n row has bit m-1 clear.
-//     The table keeps one status row per entry -- the AND of the four edges
-//     (key idea 1).
+//   DC pass (pkg/src/bitalign/distance.py:97-150): a wavefront of G lanes that
+//     covers 16 levels; lane q owns LPL = 16/G consecutive levels and at step s
+//     evaluates column j = s-q+1 of all of them, column-major inside the lane.
+//     The first of its levels takes R[d-1][j] from lane q-1 by one warp
+//     shuffle (lane 0: the carry row of the previous pass, full-width rows of
+//     its last level).  Rows are NW x 32-bit registers (W <= 32 NW).  Early
+//     termination (key idea 2): the window's DC ends with the first pass
+//     holding a level whose column-n row has bit m-1 clear.  The table keeps
+//     one status row per entry -- the AND of the four edges (key idea 1).
 //
 //   Table (key idea 3, extended to bits).  A traceback state (d, j, i) on any
 //     path from (d_min, n, m-1) satisfies |(m-1-i) - (n-j)| <= d_min - d, so
 //     every table read of entry (e, j) touches bits within d_min - e of the
 //     diagonal c_j = m-1-n+j.  When d_min <= 15 a 32-bit band around c_j holds
-//     every bit the traceback can ever read: band mode stores 32 bits per
-//     entry for levels 0..15 in shared memory.  A window needing level 16+
-//     restarts in full mode (full-width rows in a per-group global slab).
-//     W <= 32 rows are 32 bits wide and always live in shared memory.
+//     every bit the traceback can ever read: band mode stores 32 bits per entry
+//     for levels 0..15, in a per-warp global region laid out [pass][step][lane]
+//     x LPL words so each wavefront step is one coalesced 16-byte store per
+//     lane (the region stays L2-resident).  A window needing level 16+ restarts
+//     in full mode (full-width rows in a per-group global slab).  W <= 32 rows
+//     are 32 bits wide and need no band.
 //
 //   TB (pkg/src/bitalign/backtrace.py:70-167): greedy walk from
 //     (j=n, d=d_min, i=m-1), edge bits recomputed from three table reads and
-//     the symbol codes (backtrace.py:84-99), first active edge in the
-//     configured priority.  The G lanes speculate G consecutive diagonal
-//     ('=') steps at once; a ballot finds the first non-match, so a run of
-//     matches costs one round trip.  Ops are emitted in walk (= forward) order.
+//     the symbol codes (backtrace.py:84-99), first active edge by a priority
+//     LUT.  The G lanes speculate G consecutive diagonal ('=') steps at once;
+//     a ballot finds the first non-match, so a run of matches costs one round
+//     trip.  Ops are emitted in walk (= forward) order.
 //
 // Counters follow the reference's stored predicate (dptable.py:62-82) in
 // closed form; entry reads are counted per taken step.
@@ -61,6 +63,7 @@ struct KernelParams {
     uint8_t* dists;
     uint32_t* overflow;        // per-group global full-mode table slabs
     int64_t overflow_words_per_group;
+    uint32_t* band;            // per-warp global band tables
     unsigned long long* queue; // atomic pair counter
 };
 
@@ -74,18 +77,9 @@ struct LaunchShape {
     int64_t overflow_words_per_group;
 };
 
-// lock-step kernel (genasm_lockstep.cu): every group does DC, TB and setup
+// the fused kernel (genasm_lockstep.cu); group in {4, 8, 16} lanes per pair
 cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_threads,
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,
                                    size_t* cap, LaunchShape* shape);
-
-// thread-per-window column-major kernel (genasm_colmajor.cu)
-cudaError_t launch_genasm_colmajor(const KernelParams& P, int num_sms, cudaStream_t stream,
-                                   uint32_t** overflow, size_t* cap, LaunchShape* shape);
-
-// warp-specialised kernel (genasm_pipeline.cu): DC warps + traceback warps per CTA
-cudaError_t launch_genasm_ws(const KernelParams& P, int dc_warps, int num_sms,
-                             cudaStream_t stream, uint32_t** overflow, size_t* cap,
-                             LaunchShape* shape);
 
 }  // namespace genasm

@@ -1,8 +1,6 @@
-// genasm_lockstep.cu -- lock-step variant of the fused DC+TB kernel (sm_100a):
-// every group of G lanes owns one pair and runs DC, traceback and window
-// setup itself; the groups of a warp advance in pass rounds.  Kept as the
-// fallback/comparison path (GA_KERNEL=lockstep); the default is the
-// warp-specialised kernel in genasm_ws.cu.
+// genasm_lockstep.cu -- the fused windowed DC+TB kernel (sm_100a): every group
+// of G lanes owns one pair and runs DC, traceback and window setup itself;
+// the groups of a warp advance in pass rounds.  Design: genasm_kernel.cuh.
 #include "genasm_device.cuh"
 
 namespace genasm {
@@ -22,13 +20,25 @@ genasm_kernel(const KernelParams P) {
     const int gib = threadIdx.x / G;
     const int groups_per_block = blockDim.x / G;
 
-    uint32_t* tab = smem + gib * GE::GROUP_W;
-    uint32_t* carry = tab + GE::TAB_W;
+    constexpr int LPP = G * LPL;                       // levels per pass
+    constexpr int SMAX = WMAX + G - 1;                 // wavefront steps per pass
+    constexpr int NPASS = BAND ? 1 : (LV + LPP - 1) / LPP;  // band-table passes
+    // 32-word pad: the wavefront's look-ahead loads reach G*NW words before a region
+    uint32_t* carry = smem + 32 + gib * (2 * WMAX * NW + WMAX / 2);
     uint32_t* pmcol = carry + WMAX * NW;
     uint8_t* cp = reinterpret_cast<uint8_t*>(pmcol + WMAX * NW);
     uint8_t* ct = cp + WMAX;
     const int64_t gid = (int64_t)blockIdx.x * groups_per_block + gib;
     uint32_t* gtab = P.overflow + gid * P.overflow_words_per_group;
+    // this warp's band table: [pass][step][lane][LPL] words (DcLaneM)
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t* gband = P.band + wid * (int64_t)NPASS * SMAX * 32 * LPL;
+    // band word of table entry (level e, column index c = col-1): written by lane
+    // q = (e mod LPP) / LPL of the group at step c + q of pass e / LPP
+    auto bword = [&](int e, int c) -> uint32_t {
+        const int pp = e / LPP, r = e - pp * LPP, qq = r / LPL, kk = r - qq * LPL;
+        return gband[(((int64_t)pp * SMAX + c + qq) * 32 + gbase + qq) * LPL + kk];
+    };
     const int W = P.W, O = P.O, K = P.k;
     PairResult* results = reinterpret_cast<PairResult*>(P.results);
 
@@ -163,9 +173,9 @@ genasm_kernel(const KernelParams P) {
         // ================= DC pass round (all groups in lock-step) =================
         {
             const bool in_dc = phase == IN_DC;
-            constexpr int LPP = G * LPL;  // levels per pass
             DcLaneM<NW, G, LPL> L;
-            L.init(q, in_dc, pass, m, n, K, W, full, tab, carry, pmcol, gtab);
+            L.init(q, in_dc, pass, m, n, K, W, full, const_cast<uint32_t*>(gband), lane, carry,
+                   pmcol, gtab);
             // warp-uniform trip counts: fill [0, G-1), steady [G-1, nmin), drain [.., steps)
             const int steps = __reduce_max_sync(FULL, in_dc ? n + G - 1 : 0);
             const int nmin = __reduce_min_sync(FULL, in_dc ? n : WMAX);
@@ -251,9 +261,9 @@ genasm_kernel(const KernelParams P) {
                         ib = gbit(dm1, jq, iq - 1);
                     } else {
                         const int c1 = col1 > 1 ? col1 - 1 : 0;
-                        const uint32_t A = tab[d * WMAX + c1];
-                        const uint32_t Bd = tab[dm1 * WMAX + c1];
-                        const uint32_t Bu = tab[dm1 * WMAX + jq - 1];
+                        const uint32_t A = bword(d, c1);
+                        const uint32_t Bd = bword(dm1, c1);
+                        const uint32_t Bu = bword(dm1, jq - 1);
                         int a1 = cbase + col1, a2 = cbase + jq;
                         a1 = a1 < 0 ? 0 : (a1 > GE::BAND_MAX ? GE::BAND_MAX : a1);
                         a2 = a2 < 0 ? 0 : (a2 > GE::BAND_MAX ? GE::BAND_MAX : a2);
@@ -361,7 +371,7 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     KernelParams P = base;
     if (block < G || block > kMaxBlock || block % 32) block = G >= 16 ? 64 : 32;
     const int groups_per_block = block / G;
-    const int smem = groups_per_block * GE::GROUP_W * 4;
+    const int smem = (32 + groups_per_block * (2 * GE::WMAX * NW + GE::WMAX / 2)) * 4;
     auto kern = genasm_kernel<NW, G, LPL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -369,12 +379,22 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    // resident warps bound the band tables' L2 footprint (≈34 KB per warp at W=64,
+    // G=4); measured best on config 3 with occupancy-limited residency (≈24 warps)
+    const char* cap_env = getenv("GA_WARPS_PER_SM");
+    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 64;
+    const int bcap = warps_cap * 32 / block;
+    if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
     int grid = num_sms * per_sm;
     const int64_t max_useful = (P.n_pairs + groups_per_block - 1) / groups_per_block;
     if (grid > max_useful) grid = (int)(max_useful > 0 ? max_useful : 1);
     const int levels_cap = ((P.k + 1 + G * LPL - 1) / (G * LPL)) * (G * LPL);
     P.overflow_words_per_group = GE::BAND ? (int64_t)levels_cap * P.W * NW : 0;
-    const size_t need = (size_t)grid * groups_per_block * (size_t)P.overflow_words_per_group;
+    constexpr int SMAX = GE::WMAX + G - 1;
+    constexpr int NPASS = GE::BAND ? 1 : (GE::LV + G * LPL - 1) / (G * LPL);
+    const size_t slabs = (size_t)grid * groups_per_block * (size_t)P.overflow_words_per_group;
+    const size_t bands = (size_t)grid * (block / 32) * NPASS * SMAX * 32 * LPL;
+    const size_t need = slabs + bands + 64;
     if (need > *overflow_cap || !*overflow) {
         if (*overflow) cudaFree(*overflow);
         *overflow = nullptr;
@@ -384,6 +404,7 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
         *overflow_cap = need;
     }
     P.overflow = *overflow;
+    P.band = *overflow + ((slabs + 63) & ~(size_t)63);  // 256-byte aligned band region
     kern<<<grid, block, smem, stream>>>(P);
     shape->grid = grid;
     shape->block = block;
