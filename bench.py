@@ -287,31 +287,50 @@ def main():
         t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
         t.numpy()[:] = np.frombuffer(np.ascontiguousarray(a).tobytes(), dtype=np.uint8)
         return t
+    # Inputs: one code byte per symbol (what PackedBatch holds); outputs: the
+    # result records, window distances and 2-bit ops (ga_batch_out.ops2, packed
+    # on the device).  ga_align_batch pipelines chunks over three streams.
+    ops2_out = PackedResults.allocate(batch, W, O, ops2=True)
     h_in = [pinned_copy(x) for x in (batch.codes, batch.pat_off, batch.pat_len, batch.txt_off,
-                                     batch.txt_len, order, host_out.ops_off, host_out.win_off)]
+                                     batch.txt_len, ops2_out.ops_off, ops2_out.win_off)]
     h_res = torch.empty(n * 64, dtype=torch.uint8, pin_memory=True)
-    h_ops = torch.empty(host_out.ops.shape[0], dtype=torch.uint8, pin_memory=True)
+    h_ops = torch.empty(ops2_out.ops.shape[0], dtype=torch.uint8, pin_memory=True)
     h_dst = torch.empty(host_out.dists.shape[0], dtype=torch.uint8, pin_memory=True)
-    hin = _abi.GaBatchIn(n, h_in[0].data_ptr(), int(batch.codes.nbytes), h_in[1].data_ptr(),
-                         h_in[2].data_ptr(), h_in[3].data_ptr(), h_in[4].data_ptr(),
-                         h_in[5].data_ptr())
-    hout = _abi.GaBatchOut(h_res.data_ptr(), h_in[6].data_ptr(), h_ops.data_ptr(),
-                           int(h_ops.shape[0]), h_in[7].data_ptr(), h_dst.data_ptr(),
-                           int(h_dst.shape[0]))
-    h2d = sum(int(t.shape[0]) for t in h_in)
+    hin = _abi.GaBatchIn(n, h_in[0].data_ptr(), int(batch.codes.shape[0]), h_in[1].data_ptr(),
+                         h_in[2].data_ptr(), h_in[3].data_ptr(), h_in[4].data_ptr(), None)
+    hout = _abi.GaBatchOut(h_res.data_ptr(), h_in[5].data_ptr(), h_ops.data_ptr(),
+                           ops2_out.n_ops, h_in[6].data_ptr(), h_dst.data_ptr(),
+                           int(h_dst.shape[0]), 1)
+    # ga_align_batch copies the sequences, lengths, offsets and the LPT order
+    h2d = int(h_in[0].shape[0]) + sum(int(t.shape[0]) for t in h_in[1:]) + 4 * n
     d2h = int(h_res.shape[0] + h_ops.shape[0] + h_dst.shape[0])
 
-    def e2e_step():
-        rc = L.ga_align_batch(ctx, C.byref(hin), C.byref(cfg), C.byref(hout))
-        if rc != 0:
-            raise RuntimeError(L.ga_last_error(ctx).decode())
-    e2e_step()  # warm the context's own buffers
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        e2e_step()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    def e2e_run(bin_, steps):
+        def once():
+            rc = L.ga_align_batch(ctx, C.byref(bin_), C.byref(cfg), C.byref(hout))
+            if rc != 0:
+                raise RuntimeError(L.ga_last_error(ctx).decode())
+        once()  # warm the context's own buffers
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            once()
+        return max_over_ranks(time.perf_counter() - t0)
+    e2e_s = e2e_run(hin, args.e2e_steps)
     e2e_value = pairs_all * args.e2e_steps / e2e_s
+    res_bytes = h_res.numpy().copy()
+    # variant: sequences already held 2 bits per symbol on the host (ga_batch_in.packed2)
+    packed = engine.pack2(batch.codes)
+    h_pk = pinned_copy(packed.data)
+    hin_pk = _abi.GaBatchIn(n, h_pk.data_ptr(), int(batch.codes.shape[0]), h_in[1].data_ptr(),
+                            h_in[2].data_ptr(), h_in[3].data_ptr(), h_in[4].data_ptr(), None,
+                            1, int(packed.exceptions.shape[0]),
+                            packed.exceptions.ctypes.data if packed.exceptions.shape[0] else None)
+    e2e_pk_s = e2e_run(hin_pk, args.e2e_steps)
+    e2e_pk_value = pairs_all * args.e2e_steps / e2e_pk_s
+    if not np.array_equal(res_bytes, h_res.numpy()):
+        raise RuntimeError("packed-input and byte-input host runs disagree")
+    h2d_pk = h2d - int(h_in[0].shape[0]) + int(h_pk.shape[0]) + 8 * int(packed.exceptions.shape[0])
 
     # device path and host path must agree exactly
     dev_res = d_res.cpu().numpy()
@@ -369,7 +388,11 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "alignments/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                    "path": "ga_align_batch (C-ABI) on pinned host buffers"},
+                    "path": "ga_align_batch (C-ABI) on pinned host buffers: 1 byte/symbol in, "
+                            "results + distances + 2-bit ops out, chunked copy/kernel overlap",
+                    "packed_input": {"value": e2e_pk_value, "h2d_bytes_per_step": h2d_pk,
+                                     "path": "same call with ga_batch_in.packed2 (sequences "
+                                             "held 2 bits/symbol on the host; packing not timed)"}},
             "gpu_launches": launches, "clocks": clock_info,
             "extra": {"status_counts": status_counts, "windows": work.windows,
                       "dc_entries": work.entries, "tb_steps": work.tb_steps,

@@ -50,9 +50,10 @@ typedef struct {
  * All sequences live in one code array; offsets index into it. */
 typedef struct {
     int64_t        n_pairs;
-    const uint8_t* codes;      /* symbol codes 0..4 */
-    int64_t        codes_len;  /* bytes in `codes` (for host->device copies) */
-    const int64_t* pat_off;
+    const uint8_t* codes;      /* symbol codes 0..4 (one byte per symbol), or 2-bit
+                                  packed ACGT when packed2 != 0 */
+    int64_t        codes_len;  /* symbols in `codes` */
+    const int64_t* pat_off;    /* offsets and lengths are in symbols */
     const int32_t* pat_len;
     const int64_t* txt_off;
     const int32_t* txt_len;
@@ -60,6 +61,12 @@ typedef struct {
                                   0..n_pairs-1, longest first for load balance);
                                   NULL: ga_align_batch computes it on the host,
                                   ga_align_batch_device uses input order */
+    /* ga_align_batch only: 2-bit input, four symbols per byte (symbol x in
+     * bits 2(x%4)..2(x%4)+1 of byte x/4, 0..3 = ACGT); the positions of
+     * symbols outside ACGT (code 4) are listed in `exceptions` (ascending). */
+    int32_t        packed2;
+    int64_t        n_exceptions;
+    const int64_t* exceptions;
 } ga_batch_in;
 
 /* One AlignmentResult (pkg/src/bitalign/window.py:73-82) or its failure.
@@ -81,12 +88,16 @@ typedef struct {
  * distances per pair. */
 typedef struct {
     ga_pair_result* results;          /* n_pairs */
-    const int64_t*  ops_off;          /* n_pairs */
-    uint8_t*        ops;              /* ASCII '=','X','I','D' in walk (= forward) order */
-    int64_t         ops_capacity;     /* bytes in `ops` */
+    const int64_t*  ops_off;          /* n_pairs, in ops */
+    uint8_t*        ops;              /* ASCII '=','X','I','D' in walk (= forward) order,
+                                         or 2-bit op codes when ops2 != 0 */
+    int64_t         ops_capacity;     /* ops that fit in `ops` */
     const int64_t*  win_off;          /* n_pairs */
     uint8_t*        window_distances; /* AlignmentResult.window_distances, d_min per window */
     int64_t         win_capacity;     /* entries in `window_distances` */
+    /* ga_align_batch only: 2-bit ops (0 '=', 1 'X', 2 'I', 3 'D'), four per
+     * byte like packed input; every ops_off must then be a multiple of 4. */
+    int32_t         ops2;
 } ga_batch_out;
 
 typedef struct ga_ctx ga_ctx;
@@ -132,6 +143,14 @@ int64_t ga_last_launch_count(const ga_ctx* ctx);
 /* Longest-first processing order (LPT) by pattern length: the host-side
  * length bucketing that balances mixed read lengths. */
 void ga_lpt_order(int64_t n_pairs, const int32_t* pat_len, int32_t* order_out);
+
+/* Host-side format helpers (multithreaded): 2-bit packing of symbol codes
+ * into ceil(n/4) bytes; returns the number of code-4 symbols and lists the
+ * first max_exceptions of their positions (ascending) in `exceptions` (may
+ * be NULL to only count).  And 2-bit ops -> ASCII. */
+int64_t ga_pack2(const uint8_t* codes, int64_t n, uint8_t* packed, int64_t* exceptions,
+                 int64_t max_exceptions);
+void ga_unpack_ops(const uint8_t* ops2, int64_t first_op, int64_t n_ops, char* out);
 
 /* Pinned host memory for zero-staging host<->device copies (bench e2e). */
 void* ga_host_alloc(int64_t bytes);

@@ -31,13 +31,16 @@ class GaConfig(C.Structure):
 class GaBatchIn(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("codes", C.c_void_p), ("codes_len", C.c_int64),
                 ("pat_off", C.c_void_p), ("pat_len", C.c_void_p),
-                ("txt_off", C.c_void_p), ("txt_len", C.c_void_p), ("order", C.c_void_p)]
+                ("txt_off", C.c_void_p), ("txt_len", C.c_void_p), ("order", C.c_void_p),
+                ("packed2", C.c_int32), ("n_exceptions", C.c_int64),
+                ("exceptions", C.c_void_p)]
 
 
 class GaBatchOut(C.Structure):
     _fields_ = [("results", C.c_void_p), ("ops_off", C.c_void_p), ("ops", C.c_void_p),
                 ("ops_capacity", C.c_int64), ("win_off", C.c_void_p),
-                ("window_distances", C.c_void_p), ("win_capacity", C.c_int64)]
+                ("window_distances", C.c_void_p), ("win_capacity", C.c_int64),
+                ("ops2", C.c_int32)]
 
 
 # ga_pair_result, 64 bytes
@@ -116,11 +119,32 @@ class PackedBatch:
                    pat_off=starts[0::2].copy(), pat_len=pat_len,
                    txt_off=starts[1::2].copy(), txt_len=txt_len)
 
-    def struct(self, order: np.ndarray | None = None) -> GaBatchIn:
-        return GaBatchIn(self.n_pairs, self.codes.ctypes.data, int(self.codes.nbytes),
-                         self.pat_off.ctypes.data, self.pat_len.ctypes.data,
-                         self.txt_off.ctypes.data, self.txt_len.ctypes.data,
-                         None if order is None else order.ctypes.data)
+    def struct(self, order: np.ndarray | None = None,
+               packed: "Packed2 | None" = None) -> GaBatchIn:
+        """ga_batch_in over these arrays; with `packed`, the sequences travel
+        as 2-bit symbols plus the exception list (offsets stay in symbols)."""
+        s = GaBatchIn(self.n_pairs, self.codes.ctypes.data, int(self.codes.shape[0]),
+                      self.pat_off.ctypes.data, self.pat_len.ctypes.data,
+                      self.txt_off.ctypes.data, self.txt_len.ctypes.data,
+                      None if order is None else order.ctypes.data)
+        if packed is not None:
+            s.codes = packed.data.ctypes.data
+            s.packed2 = 1
+            s.n_exceptions = int(packed.exceptions.shape[0])
+            s.exceptions = packed.exceptions.ctypes.data if packed.exceptions.shape[0] else None
+        return s
+
+
+@dataclass
+class Packed2:
+    """2-bit transfer form of a code array (ga_batch_in.packed2): symbol x in
+    bits 2(x%4).. of byte x/4, code-4 positions listed in `exceptions`."""
+
+    data: np.ndarray        # uint8, ceil(n/4)
+    exceptions: np.ndarray  # int64, ascending
+
+
+_OPS_LUT = np.frombuffer(b"=XID", dtype=np.uint8)
 
 
 @dataclass
@@ -128,15 +152,20 @@ class PackedResults:
     """Host-side outputs: the ``ga_batch_out`` arrays."""
 
     results: np.ndarray   # RESULT_DTYPE
-    ops_off: np.ndarray   # int64
-    ops: np.ndarray       # uint8 ASCII
+    ops_off: np.ndarray   # int64, in ops
+    ops: np.ndarray       # uint8: ASCII ops, or 2-bit ops (four per byte) when ops2
     win_off: np.ndarray   # int64
     dists: np.ndarray     # uint8
+    ops2: bool = False
+    n_ops: int = 0        # ops capacity
 
     @classmethod
-    def allocate(cls, batch: PackedBatch, window: int, overlap: int) -> "PackedResults":
+    def allocate(cls, batch: PackedBatch, window: int, overlap: int,
+                 ops2: bool = False) -> "PackedResults":
         n = batch.n_pairs
         cap = batch.pat_len.astype(np.int64) + batch.txt_len.astype(np.int64)
+        if ops2:  # every pair's ops start on a byte boundary
+            cap = (cap + 3) & ~np.int64(3)
         ops_off = np.zeros(n, dtype=np.int64)
         if n:
             np.cumsum(cap[:-1], out=ops_off[1:])
@@ -144,18 +173,26 @@ class PackedResults:
         win_off = np.zeros(n, dtype=np.int64)
         if n:
             np.cumsum(nwin[:-1], out=win_off[1:])
+        total = int(cap.sum())
+        nbytes = (total + 3) // 4 if ops2 else total
         return cls(results=np.zeros(n, dtype=RESULT_DTYPE), ops_off=ops_off,
-                   ops=np.zeros(max(1, int(cap.sum())), dtype=np.uint8), win_off=win_off,
-                   dists=np.zeros(max(1, int(nwin.sum())), dtype=np.uint8))
+                   ops=np.zeros(max(1, nbytes), dtype=np.uint8), win_off=win_off,
+                   dists=np.zeros(max(1, int(nwin.sum())), dtype=np.uint8), ops2=ops2,
+                   n_ops=total)
 
     def struct(self) -> GaBatchOut:
         return GaBatchOut(self.results.ctypes.data, self.ops_off.ctypes.data,
-                          self.ops.ctypes.data, int(self.ops.nbytes), self.win_off.ctypes.data,
-                          self.dists.ctypes.data, int(self.dists.nbytes))
+                          self.ops.ctypes.data, self.n_ops, self.win_off.ctypes.data,
+                          self.dists.ctypes.data, int(self.dists.nbytes), int(self.ops2))
 
     def cigar(self, q: int) -> str:
         off = int(self.ops_off[q])
-        return self.ops[off:off + int(self.results["ops_len"][q])].tobytes().decode("ascii")
+        n_ops = int(self.results["ops_len"][q])
+        if self.ops2:
+            b = self.ops[off // 4:(off + n_ops + 3) // 4]
+            codes = (b[:, None] >> np.array([0, 2, 4, 6], dtype=np.uint8)) & 3
+            return _OPS_LUT[codes.reshape(-1)[:n_ops]].tobytes().decode("ascii")
+        return self.ops[off:off + n_ops].tobytes().decode("ascii")
 
     def distances(self, q: int, pattern_len: int, window: int, overlap: int) -> tuple[int, ...]:
         off = int(self.win_off[q])

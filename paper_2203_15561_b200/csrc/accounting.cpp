@@ -36,7 +36,13 @@ void ga_work_stats(const ga_batch_in* in, const ga_config* cfg, const ga_batch_o
                 const ga_pair_result& r = out->results[q];
                 if (r.status != GA_OK) continue;
                 const int64_t Lp = in->pat_len[q], Lt = in->txt_len[q];
-                const uint8_t* ops = out->ops + out->ops_off[q];
+                const int64_t o0 = out->ops_off[q];
+                // op x of the pair: ASCII, or 2-bit codes (0 '=', 1 'X', 2 'I', 3 'D')
+                auto op_at = [&](int64_t x) -> uint8_t {
+                    if (!out->ops2) return out->ops[o0 + x];
+                    const int64_t y = o0 + x;
+                    return "=XID"[(out->ops[y >> 2] >> (2 * (y & 3))) & 3];
+                };
                 const uint8_t* dist = out->window_distances + out->win_off[q];
                 const int64_t nwin = ga_num_windows(Lp, W, O);
                 int64_t pos = 0, t = 0;
@@ -53,7 +59,7 @@ void ga_work_stats(const ga_batch_in* in, const ga_config* cfg, const ga_batch_o
                     // walk this window's ops
                     int64_t consumed = 0;
                     while (pos < r.ops_len && consumed < budget) {
-                        const uint8_t op = ops[pos++];
+                        const uint8_t op = op_at(pos++);
                         if (op != 'D') consumed++;
                         if (op != 'I') t++;
                         acc.tb_steps++;

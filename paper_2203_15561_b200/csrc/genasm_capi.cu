@@ -6,6 +6,11 @@
 // process pool), longest-first ordering, device buffer management and the
 // host<->device copies.  One context per device; contexts are independent,
 // so a multi-GPU caller runs one host thread per context.
+//
+// The host-buffer call (ga_align_batch) splits the batch into chunks of
+// consecutive pairs and pipelines them over three streams: the H2D of chunk
+// k+1 and the D2H of chunk k-1 overlap the kernel of chunk k.  Sequences can
+// travel 2 bits per symbol and ops 2 bits per op.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +23,12 @@
 
 #include "../../include/genasm.h"
 #include "genasm_kernel.cuh"
+
+namespace genasm {
+cudaError_t launch_unpack2(const uint8_t* packed, int64_t nsym, uint8_t* out, cudaStream_t st);
+cudaError_t launch_patch(const int64_t* pos, int64_t n, int64_t base, uint8_t* out, cudaStream_t st);
+cudaError_t launch_pack_ops(const uint8_t* ascii, int64_t nops, uint8_t* out, cudaStream_t st);
+}  // namespace genasm
 
 struct DevBuf {
     void* ptr = nullptr;
@@ -39,17 +50,32 @@ struct DevBuf {
     }
 };
 
+// device buffers and chunk-local host arrays of one pipeline slot
+struct Slot {
+    DevBuf codes, packed, exc, pat_off, pat_len, txt_off, txt_len, order, results, ops_off, ops,
+        ops2, win_off, dists;
+    std::vector<int64_t> h_pat_off, h_txt_off, h_ops_off, h_win_off, h_exc;
+    std::vector<int32_t> h_order;
+    cudaEvent_t in_done = nullptr, out_done = nullptr, kern_done = nullptr;
+    void release() {
+        for (DevBuf* b : {&codes, &packed, &exc, &pat_off, &pat_len, &txt_off, &txt_len, &order,
+                          &results, &ops_off, &ops, &ops2, &win_off, &dists})
+            b->release();
+        for (cudaEvent_t ev : {in_done, out_done, kern_done})
+            if (ev) cudaEventDestroy(ev);
+    }
+};
+
 struct ga_ctx {
     int device = 0;
     int num_sms = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
     std::string err;
     int64_t launches = 0;
     unsigned long long* queue = nullptr;
     uint32_t* overflow = nullptr;
     size_t overflow_cap = 0;
-    DevBuf codes, pat_off, pat_len, txt_off, txt_len, order, results, ops_off, ops, win_off, dists;
-    std::vector<int32_t> host_order;
+    Slot slot[2];
     genasm::LaunchShape last_shape{};
 };
 
@@ -142,7 +168,11 @@ int ga_create(int device, ga_ctx** out) {
     ga_ctx* c = new ga_ctx();
     c->device = device;
     e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (cudaStream_t* s : {&c->stream, &c->stream_in, &c->stream_out})
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    for (Slot& sl : c->slot)
+        for (cudaEvent_t* ev : {&sl.in_done, &sl.out_done, &sl.kern_done})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&c->queue, sizeof(unsigned long long));
     if (e != cudaSuccess) {
         delete c;
@@ -155,12 +185,12 @@ int ga_create(int device, ga_ctx** out) {
 void ga_destroy(ga_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (DevBuf* b : {&c->codes, &c->pat_off, &c->pat_len, &c->txt_off, &c->txt_len, &c->order,
-                      &c->results, &c->ops_off, &c->ops, &c->win_off, &c->dists})
-        b->release();
+    cudaDeviceSynchronize();
+    for (Slot& sl : c->slot) sl.release();
     if (c->overflow) cudaFree(c->overflow);
     if (c->queue) cudaFree(c->queue);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    for (cudaStream_t s : {c->stream, c->stream_in, c->stream_out})
+        if (s) cudaStreamDestroy(s);
     delete c;
 }
 
@@ -245,63 +275,169 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     const int64_t n = in->n_pairs;
     c->launches = 0;
     if (n <= 0) return 0;
+    if (out->ops2) {
+        for (int64_t q = 0; q < n; ++q)
+            if (out->ops_off[q] & 3) {
+                c->err = "ops2 output needs every ops_off to be a multiple of 4";
+                return -3;
+            }
+    }
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
-    cudaStream_t st = c->stream;
-    const int32_t* order = in->order;
-    if (!order) {
-        c->host_order.resize((size_t)n);
-        ga_lpt_order(n, in->pat_len, c->host_order.data());
-        order = c->host_order.data();
+
+    // ---- chunk plan: consecutive pairs; 2 chunks overlap copies with the kernel
+    // when the batch is large enough that each chunk still fills the GPU ----
+    int chunks = env_int("GA_CHUNKS", n >= 65536 ? 2 : 1);
+    if (chunks < 1) chunks = 1;
+    if (chunks > n) chunks = (int)n;
+    // chunking needs output offsets that grow with the input index (the
+    // prefix-sum layout every caller in this package uses)
+    for (int64_t q = 1; q < n && chunks > 1; ++q)
+        if (out->ops_off[q] < out->ops_off[q - 1] || out->win_off[q] < out->win_off[q - 1])
+            chunks = 1;
+    int64_t launches = 0;
+    for (int k = 0; k < chunks; ++k) {
+        const int64_t q0 = n * k / chunks, q1 = n * (k + 1) / chunks;
+        const int64_t m = q1 - q0;
+        Slot& S = c->slot[k & 1];
+        // the symbol, op and window ranges the chunk touches
+        int64_t lo = INT64_MAX, hi = 0;
+        for (int64_t q = q0; q < q1; ++q) {
+            lo = std::min(lo, std::min(in->pat_off[q], in->txt_off[q]));
+            hi = std::max(hi, std::max(in->pat_off[q] + in->pat_len[q], in->txt_off[q] + in->txt_len[q]));
+        }
+        if (lo > hi) lo = hi;
+        int64_t olo = INT64_MAX, ohi = 0, wlo = INT64_MAX, whi = 0;
+        for (int64_t q = q0; q < q1; ++q) {
+            olo = std::min(olo, out->ops_off[q]);
+            wlo = std::min(wlo, out->win_off[q]);
+        }
+        // a pair's capacity ends where the next larger offset (or the buffer) begins
+        ohi = out->ops_capacity;
+        whi = out->win_capacity;
+        for (int64_t q = 0; q < n; ++q) {
+            if (q >= q0 && q < q1) continue;
+            if (out->ops_off[q] >= olo) ohi = std::min(ohi, out->ops_off[q]);
+            if (out->win_off[q] >= wlo) whi = std::min(whi, out->win_off[q]);
+        }
+        const int64_t base = in->packed2 ? (lo & ~int64_t(3)) : lo;
+        const int64_t nsym = hi - base;
+        // chunk-local host arrays (rebased offsets, LPT order)
+        S.h_pat_off.resize((size_t)m);
+        S.h_txt_off.resize((size_t)m);
+        S.h_ops_off.resize((size_t)m);
+        S.h_win_off.resize((size_t)m);
+        S.h_order.resize((size_t)m);
+        for (int64_t q = 0; q < m; ++q) {
+            S.h_pat_off[(size_t)q] = in->pat_off[q0 + q] - base;
+            S.h_txt_off[(size_t)q] = in->txt_off[q0 + q] - base;
+            S.h_ops_off[(size_t)q] = out->ops_off[q0 + q] - olo;
+            S.h_win_off[(size_t)q] = out->win_off[q0 + q] - wlo;
+        }
+        if (in->order && chunks == 1) {
+            std::copy(in->order, in->order + n, S.h_order.begin());
+        } else {
+            ga_lpt_order(m, in->pat_len + q0, S.h_order.data());
+        }
+        int64_t nexc = 0, exc0 = 0;
+        if (in->packed2 && in->n_exceptions > 0) {
+            exc0 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions, base) -
+                   in->exceptions;
+            const int64_t exc1 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions,
+                                                  hi) - in->exceptions;
+            nexc = exc1 - exc0;
+        }
+        const int64_t nops = ohi - olo;
+        const int64_t nwin = whi - wlo;
+        if ((e = S.codes.ensure((size_t)nsym + 16)) || (e = S.pat_off.ensure((size_t)m * 8)) ||
+            (e = S.txt_off.ensure((size_t)m * 8)) || (e = S.pat_len.ensure((size_t)m * 4)) ||
+            (e = S.txt_len.ensure((size_t)m * 4)) || (e = S.order.ensure((size_t)m * 4)) ||
+            (e = S.ops_off.ensure((size_t)m * 8)) || (e = S.win_off.ensure((size_t)m * 8)) ||
+            (e = S.results.ensure((size_t)m * sizeof(ga_pair_result))) ||
+            (e = S.ops.ensure((size_t)nops + 16)) || (e = S.dists.ensure((size_t)nwin + 16)))
+            return fail(c, e, "cudaMalloc");
+        if (in->packed2 && ((e = S.packed.ensure((size_t)(nsym + 3) / 4 + 16)) ||
+                            (e = S.exc.ensure((size_t)(nexc > 0 ? nexc : 1) * 8))))
+            return fail(c, e, "cudaMalloc");
+        if (out->ops2 && (e = S.ops2.ensure((size_t)(nops + 3) / 4 + 16)))
+            return fail(c, e, "cudaMalloc");
+
+        // ---- H2D (input stream), after this slot's previous chunk left the device ----
+        cudaStream_t si = c->stream_in, sk = c->stream, so = c->stream_out;
+        if (k >= 2 && (e = cudaStreamWaitEvent(si, S.out_done, 0))) return fail(c, e, "wait");
+        auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+            return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, si) : cudaSuccess;
+        };
+        if (in->packed2) {
+            e = h2d(S.packed.ptr, in->codes + base / 4, (size_t)(nsym + 3) / 4);
+            if (!e && nexc) e = h2d(S.exc.ptr, in->exceptions + exc0, (size_t)nexc * 8);
+        } else {
+            e = h2d(S.codes.ptr, in->codes + base, (size_t)nsym);
+        }
+        if (!e) e = h2d(S.pat_off.ptr, S.h_pat_off.data(), (size_t)m * 8);
+        if (!e) e = h2d(S.txt_off.ptr, S.h_txt_off.data(), (size_t)m * 8);
+        if (!e) e = h2d(S.pat_len.ptr, in->pat_len + q0, (size_t)m * 4);
+        if (!e) e = h2d(S.txt_len.ptr, in->txt_len + q0, (size_t)m * 4);
+        if (!e) e = h2d(S.order.ptr, S.h_order.data(), (size_t)m * 4);
+        if (!e) e = h2d(S.ops_off.ptr, S.h_ops_off.data(), (size_t)m * 8);
+        if (!e) e = h2d(S.win_off.ptr, S.h_win_off.data(), (size_t)m * 8);
+        if (!e) e = cudaEventRecord(S.in_done, si);
+        if (e) return fail(c, e, "H2D copy");
+
+        // ---- compute stream: expand 2-bit sequences, align, pack ops ----
+        if ((e = cudaStreamWaitEvent(sk, S.in_done, 0))) return fail(c, e, "wait");
+        if (in->packed2) {
+            if ((e = genasm::launch_unpack2((const uint8_t*)S.packed.ptr, nsym, (uint8_t*)S.codes.ptr,
+                                            sk)) ||
+                (e = genasm::launch_patch((const int64_t*)S.exc.ptr, nexc, base, (uint8_t*)S.codes.ptr,
+                                          sk)))
+                return fail(c, e, "unpack kernel");
+            launches += 1 + (nexc > 0);
+        }
+        ga_batch_in din{};
+        din.n_pairs = m;
+        din.codes = (const uint8_t*)S.codes.ptr;
+        din.codes_len = nsym;
+        din.pat_off = (const int64_t*)S.pat_off.ptr;
+        din.pat_len = (const int32_t*)S.pat_len.ptr;
+        din.txt_off = (const int64_t*)S.txt_off.ptr;
+        din.txt_len = (const int32_t*)S.txt_len.ptr;
+        din.order = (const int32_t*)S.order.ptr;
+        ga_batch_out dout{};
+        dout.results = (ga_pair_result*)S.results.ptr;
+        dout.ops_off = (const int64_t*)S.ops_off.ptr;
+        dout.ops = (uint8_t*)S.ops.ptr;
+        dout.ops_capacity = nops;
+        dout.win_off = (const int64_t*)S.win_off.ptr;
+        dout.window_distances = (uint8_t*)S.dists.ptr;
+        dout.win_capacity = nwin;
+        int rc = ga_align_batch_device(c, &din, cfg, &dout, sk);
+        if (rc) return rc;
+        launches += c->launches;
+        if (out->ops2) {
+            if ((e = genasm::launch_pack_ops((const uint8_t*)S.ops.ptr, nops, (uint8_t*)S.ops2.ptr, sk)))
+                return fail(c, e, "pack kernel");
+            launches += 1;
+        }
+        if ((e = cudaEventRecord(S.kern_done, sk))) return fail(c, e, "record");
+
+        // ---- D2H (output stream) ----
+        if ((e = cudaStreamWaitEvent(so, S.kern_done, 0))) return fail(c, e, "wait");
+        auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+            return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, so) : cudaSuccess;
+        };
+        e = d2h(out->results + q0, S.results.ptr, (size_t)m * sizeof(ga_pair_result));
+        if (!e) {
+            if (out->ops2) e = d2h(out->ops + olo / 4, S.ops2.ptr, (size_t)(nops + 3) / 4);
+            else e = d2h(out->ops + olo, S.ops.ptr, (size_t)nops);
+        }
+        if (!e) e = d2h(out->window_distances + wlo, S.dists.ptr, (size_t)nwin);
+        if (!e) e = cudaEventRecord(S.out_done, so);
+        if (e) return fail(c, e, "D2H copy");
     }
-    struct Cp {
-        DevBuf* buf;
-        const void* src;
-        size_t bytes;
-    } h2d[] = {
-        {&c->codes, in->codes, (size_t)in->codes_len},
-        {&c->pat_off, in->pat_off, (size_t)n * 8},
-        {&c->pat_len, in->pat_len, (size_t)n * 4},
-        {&c->txt_off, in->txt_off, (size_t)n * 8},
-        {&c->txt_len, in->txt_len, (size_t)n * 4},
-        {&c->order, order, (size_t)n * 4},
-        {&c->ops_off, out->ops_off, (size_t)n * 8},
-        {&c->win_off, out->win_off, (size_t)n * 8},
-    };
-    for (auto& x : h2d) {
-        if ((e = x.buf->ensure(x.bytes)) != cudaSuccess) return fail(c, e, "cudaMalloc");
-        if (x.bytes && (e = cudaMemcpyAsync(x.buf->ptr, x.src, x.bytes, cudaMemcpyHostToDevice,
-                                            st)) != cudaSuccess)
-            return fail(c, e, "H2D copy");
-    }
-    if ((e = c->results.ensure((size_t)n * sizeof(ga_pair_result))) != cudaSuccess ||
-        (e = c->ops.ensure((size_t)out->ops_capacity)) != cudaSuccess ||
-        (e = c->dists.ensure((size_t)out->win_capacity)) != cudaSuccess)
-        return fail(c, e, "cudaMalloc");
-    ga_batch_in din = *in;
-    din.codes = (const uint8_t*)c->codes.ptr;
-    din.pat_off = (const int64_t*)c->pat_off.ptr;
-    din.pat_len = (const int32_t*)c->pat_len.ptr;
-    din.txt_off = (const int64_t*)c->txt_off.ptr;
-    din.txt_len = (const int32_t*)c->txt_len.ptr;
-    din.order = (const int32_t*)c->order.ptr;
-    ga_batch_out dout = *out;
-    dout.results = (ga_pair_result*)c->results.ptr;
-    dout.ops_off = (const int64_t*)c->ops_off.ptr;
-    dout.ops = (uint8_t*)c->ops.ptr;
-    dout.win_off = (const int64_t*)c->win_off.ptr;
-    dout.window_distances = (uint8_t*)c->dists.ptr;
-    int rc = ga_align_batch_device(c, &din, cfg, &dout, st);
-    if (rc) return rc;
-    if ((e = cudaMemcpyAsync(out->results, dout.results, (size_t)n * sizeof(ga_pair_result),
-                             cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(out->ops, dout.ops, (size_t)out->ops_capacity,
-                             cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(out->window_distances, dout.window_distances,
-                             (size_t)out->win_capacity, cudaMemcpyDeviceToHost, st)) !=
-            cudaSuccess)
-        return fail(c, e, "D2H copy");
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail(c, e, "kernel execution");
+    if ((e = cudaStreamSynchronize(c->stream_out)) != cudaSuccess)
+        return fail(c, e, "kernel execution");
+    c->launches = launches;
     return 0;
 }
 

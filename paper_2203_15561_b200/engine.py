@@ -57,6 +57,8 @@ def lib():
             "ga_align_batch_device": ([C.c_void_p, B, F, O, C.c_void_p], C.c_int),
             "ga_last_launch_count": ([C.c_void_p], C.c_int64),
             "ga_lpt_order": ([C.c_int64, C.c_void_p, C.c_void_p], None),
+            "ga_pack2": ([C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64], C.c_int64),
+            "ga_unpack_ops": ([C.c_void_p, C.c_int64, C.c_int64, C.c_void_p], None),
             "ga_host_alloc": ([C.c_int64], C.c_void_p),
             "ga_host_free": ([C.c_void_p], None),
         }
@@ -98,16 +100,34 @@ def lpt_order(pat_len: np.ndarray) -> np.ndarray:
     return order
 
 
+def pack2(codes: np.ndarray) -> _abi.Packed2:
+    """2-bit transfer form of a code array (ga_pack2, multithreaded)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = int(codes.shape[0])
+    data = np.zeros(max(1, (n + 3) // 4), dtype=np.uint8)
+    L = lib()
+    exc = np.empty(1024, dtype=np.int64)
+    n_exc = L.ga_pack2(codes.ctypes.data, n, data.ctypes.data, exc.ctypes.data, exc.shape[0])
+    if n_exc > exc.shape[0]:
+        exc = np.empty(n_exc, dtype=np.int64)
+        L.ga_pack2(codes.ctypes.data, n, data.ctypes.data, exc.ctypes.data, n_exc)
+    exc = exc[:n_exc].copy()
+    return _abi.Packed2(data=data, exceptions=exc)
+
+
 def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: str,
-               device: int | None = None) -> PackedResults:
-    """One ga_align_batch call on one device (host buffers in and out)."""
+               device: int | None = None, *, packed2: bool = False,
+               ops2: bool = False) -> PackedResults:
+    """One ga_align_batch call on one device (host buffers in and out).
+    packed2 / ops2 select the 2-bit transfer formats of include/genasm.h."""
     dev = _default_device() if device is None else int(device)
     ctx = context(dev)
-    out = PackedResults.allocate(batch, window, overlap)
+    out = PackedResults.allocate(batch, window, overlap, ops2=ops2)
     if batch.n_pairs == 0:
         return out
     cfg = _abi.make_config(window, overlap, k, priority)
-    bin_ = batch.struct()
+    packed = pack2(batch.codes) if packed2 else None  # must outlive the call
+    bin_ = batch.struct(packed=packed)
     bout = out.struct()
     with _ctx_locks[dev]:
         rc = lib().ga_align_batch(ctx, C.byref(bin_), C.byref(cfg), C.byref(bout))
@@ -142,7 +162,11 @@ def _scatter(full: PackedResults, part: PackedResults, idx: np.ndarray, batch: P
         n_ops = int(part.results["ops_len"][local])
         src = int(part.ops_off[local])
         dst = int(full.ops_off[q])
-        full.ops[dst:dst + n_ops] = part.ops[src:src + n_ops]
+        if part.ops2:  # both layouts start every pair on a byte boundary
+            nb = (n_ops + 3) // 4
+            full.ops[dst // 4:dst // 4 + nb] = part.ops[src // 4:src // 4 + nb]
+        else:
+            full.ops[dst:dst + n_ops] = part.ops[src:src + n_ops]
         w_src = int(part.win_off[local])
         w_dst = int(full.win_off[q])
         w_n = (int(part.win_off[local + 1]) if local + 1 < len(idx) else part.dists.shape[0]) - w_src

@@ -142,6 +142,34 @@ def test_capi_host_functions():
     assert engine.lpt_order(lens).tolist() == [1, 3, 0, 2]
 
 
+def test_transfer_formats_host_side():
+    """ga_pack2 (2-bit input + exception list) and the ops2 decoders."""
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 3, 4, 5, 1023, 100_003, 2_000_003):
+        codes = rng.integers(0, 4, n).astype(np.uint8)
+        codes[rng.random(n) < 0.01] = 4
+        p = engine.pack2(codes)
+        assert p.data.shape[0] == max(1, (n + 3) // 4)
+        unpacked = ((p.data[:, None] >> np.array([0, 2, 4, 6], np.uint8)) & 3).reshape(-1)[:n]
+        assert np.array_equal(unpacked, codes & 3)
+        assert np.array_equal(p.exceptions, np.nonzero(codes == 4)[0])
+    # 2-bit ops -> ASCII, both the C decoder and PackedResults.cigar
+    ops = rng.integers(0, 4, 37).astype(np.uint8)
+    ops2 = np.zeros(10, np.uint8)
+    for x, v in enumerate(ops):
+        ops2[x // 4] |= v << (2 * (x % 4))
+    out = C.create_string_buffer(37 - 5)
+    engine.lib().ga_unpack_ops(ops2.ctypes.data, 5, 37 - 5, out)
+    expect = bytes(b"=XID"[v] for v in ops)
+    assert out.raw == expect[5:]
+    batch = _abi.PackedBatch.from_pairs([("ACGTACGTAC", "ACGTACGTACGTACGTACGTACGTACGT")])
+    res = _abi.PackedResults.allocate(batch, 64, 24, ops2=True)
+    assert res.n_ops == 40 and res.ops.shape[0] == 10
+    res.ops[:] = ops2
+    res.results["ops_len"][0] = 37
+    assert res.cigar(0) == expect.decode()
+
+
 def test_no_cpu_fallback_when_extension_missing(monkeypatch, tmp_path):
     monkeypatch.setattr(engine, "SO_PATH", str(tmp_path / "missing.so"))
     monkeypatch.setattr(engine, "_lib", None)

@@ -170,3 +170,64 @@ def test_batch_composition_invariance(gpu):
     for idx in split_lpt(batch.pat_len, 64, 24, 3):
         part = run_packed(_subset(batch, idx), 64, 24, 64, "MSID")
         assert np.array_equal(part.results, full.results[idx])
+
+
+def _with_exceptions(batch, rate=0.002, seed=5):
+    """A copy of `batch` with some symbols replaced by code 4 (non-ACGT)."""
+    from paper_2203_15561_b200._abi import PackedBatch
+    rng = np.random.default_rng(seed)
+    codes = batch.codes.copy()
+    hit = rng.random(codes.shape[0]) < rate
+    codes[hit] = 4
+    return PackedBatch(codes=codes, pat_off=batch.pat_off, pat_len=batch.pat_len,
+                       txt_off=batch.txt_off, txt_len=batch.txt_len)
+
+
+@pytest.mark.parametrize("packed2,ops2", [(True, False), (False, True), (True, True)])
+def test_transfer_formats(gpu, oracle_mod, packed2, ops2):
+    """2-bit input (with code-4 exceptions) and 2-bit ops give identical results."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(5, count=2000)
+    batch = _with_exceptions(batch)
+    got = run_packed(batch, 64, 24, 64, "MSID", packed2=packed2, ops2=ops2)
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    assert np.array_equal(got.results, exp.results)
+    assert np.array_equal(got.dists, exp.dists)
+    for q in range(batch.n_pairs):
+        n = int(exp.results["ops_len"][q])
+        o = int(exp.ops_off[q])
+        assert got.cigar(q) == exp.ops[o:o + n].tobytes().decode(), q
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 3, 7])
+def test_chunked_pipeline(gpu, monkeypatch, chunks):
+    """Chunked, stream-overlapped host path == one-shot path (ga_align_batch)."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(5, count=1500)
+    monkeypatch.setenv("GA_CHUNKS", "1")
+    ref = run_packed(batch, 64, 24, 64, "MSID")
+    monkeypatch.setenv("GA_CHUNKS", str(chunks))
+    for packed2, ops2 in [(False, False), (True, True)]:
+        got = run_packed(batch, 64, 24, 64, "MSID", packed2=packed2, ops2=ops2)
+        assert np.array_equal(got.results, ref.results)
+        assert np.array_equal(got.dists, ref.dists)
+        for q in range(0, batch.n_pairs, 7):
+            assert got.cigar(q) == ref.cigar(q)
+
+
+def test_config3_full_vs_oracle(gpu, oracle_mod):
+    """The bench workload itself: all 138,929 pairs of config 3, every field
+    against the oracle (the reference's golden digests pin the prefix)."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(3)
+    got = run_packed(batch, 64, 24, 64, "MSID", packed2=True, ops2=True)
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    assert np.array_equal(got.results, exp.results)
+    assert np.array_equal(got.dists, exp.dists)
+    for q in range(0, batch.n_pairs, 97):
+        assert got.cigar(q) == exp.ops[int(exp.ops_off[q]):int(exp.ops_off[q])
+                                       + int(exp.results["ops_len"][q])].tobytes().decode(), q
+    assert (got.results["status"] == 0).all()  # k = W: every window aligns
