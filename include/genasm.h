@@ -93,7 +93,8 @@ typedef struct {
                                          or 2-bit op codes when ops2 != 0 */
     int64_t         ops_capacity;     /* ops that fit in `ops` */
     const int64_t*  win_off;          /* n_pairs */
-    uint8_t*        window_distances; /* AlignmentResult.window_distances, d_min per window */
+    uint8_t*        window_distances; /* AlignmentResult.window_distances, d_min per window;
+                                         0 for the windows a failed pair did not complete */
     int64_t         win_capacity;     /* entries in `window_distances` */
     /* ga_align_batch only: 2-bit ops (0 '=', 1 'X', 2 'I', 3 'D'), four per
      * byte like packed input; every ops_off must then be a multiple of 4. */
@@ -125,9 +126,11 @@ void ga_destroy(ga_ctx* ctx);
 const char* ga_last_error(const ga_ctx* ctx);
 
 /* align_batch (pkg/src/bitalign/window.py:152-163) over HOST buffers:
- * host->device copies, the fused DC+TB kernel, device->host copies, all on
- * the context's stream; returns when the results are in `out`.  Results are
- * in input order and independent of batch composition. */
+ * host->device copies, the fused DC+TB kernel, device->host copies, pipelined
+ * over chunks of consecutive pairs (copy-in / kernels / copy-out on separate
+ * streams; GA_CHUNKS overrides the chunk count); returns when the results are
+ * in `out`.  Results are in input order and independent of batch composition.
+ * Pinned host buffers (ga_host_alloc) make the copies asynchronous. */
 int ga_align_batch(ga_ctx* ctx, const ga_batch_in* in, const ga_config* cfg,
                    ga_batch_out* out);
 

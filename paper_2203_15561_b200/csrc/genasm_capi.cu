@@ -50,21 +50,46 @@ struct DevBuf {
     }
 };
 
-// device buffers and chunk-local host arrays of one pipeline slot
-struct Slot {
-    DevBuf codes, packed, exc, pat_off, pat_len, txt_off, txt_len, order, results, ops_off, ops,
-        ops2, win_off, dists;
-    std::vector<int64_t> h_pat_off, h_txt_off, h_ops_off, h_win_off, h_exc;
-    std::vector<int32_t> h_order;
-    cudaEvent_t in_done = nullptr, out_done = nullptr, kern_done = nullptr;
+// Scratch one kernel launch owns: the work queue head and the overflow slabs
+// + band tables.  Chunks in flight on different slots use different scratch,
+// so their kernels can overlap (the next chunk fills SMs as one drains).
+struct Scratch {
+    unsigned long long* queue = nullptr;
+    uint32_t* overflow = nullptr;
+    size_t overflow_cap = 0;
     void release() {
-        for (DevBuf* b : {&codes, &packed, &exc, &pat_off, &pat_len, &txt_off, &txt_len, &order,
-                          &results, &ops_off, &ops, &ops2, &win_off, &dists})
-            b->release();
-        for (cudaEvent_t ev : {in_done, out_done, kern_done})
-            if (ev) cudaEventDestroy(ev);
+        if (overflow) cudaFree(overflow);
+        if (queue) cudaFree(queue);
+        overflow = nullptr;
+        queue = nullptr;
+        overflow_cap = 0;
     }
 };
+
+// One pipeline slot of the host-buffer path: device buffers, a pinned staging
+// area for the chunk's per-pair metadata, its kernel stream and events.
+// Metadata layout (host staging and device `meta` alike), per chunk of m pairs:
+//   int64 pat_off[m] | txt_off[m] | ops_off[m] | win_off[m] | int32 pat_len[m] | txt_len[m] | order[m]
+struct Slot {
+    DevBuf codes, packed, exc, meta, results, ops, ops2, dists;
+    void* h_meta = nullptr;
+    size_t h_meta_cap = 0;
+    Scratch scratch;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t in_done = nullptr, out_done = nullptr, kern_done = nullptr;
+    bool used = false;  // in_done/out_done have been recorded
+    void release() {
+        for (DevBuf* b : {&codes, &packed, &exc, &meta, &results, &ops, &ops2, &dists}) b->release();
+        if (h_meta) cudaFreeHost(h_meta);
+        h_meta = nullptr;
+        scratch.release();
+        for (cudaEvent_t ev : {in_done, out_done, kern_done})
+            if (ev) cudaEventDestroy(ev);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+constexpr int kSlots = 3;
 
 struct ga_ctx {
     int device = 0;
@@ -72,10 +97,8 @@ struct ga_ctx {
     cudaStream_t stream = nullptr, stream_in = nullptr, stream_out = nullptr;
     std::string err;
     int64_t launches = 0;
-    unsigned long long* queue = nullptr;
-    uint32_t* overflow = nullptr;
-    size_t overflow_cap = 0;
-    Slot slot[2];
+    Scratch scratch;  // ga_align_batch_device
+    Slot slot[kSlots];
     genasm::LaunchShape last_shape{};
 };
 
@@ -170,12 +193,13 @@ int ga_create(int device, ga_ctx** out) {
     e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     for (cudaStream_t* s : {&c->stream, &c->stream_in, &c->stream_out})
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    for (Slot& sl : c->slot)
+    for (Slot& sl : c->slot) {
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
         for (cudaEvent_t* ev : {&sl.in_done, &sl.out_done, &sl.kern_done})
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaMalloc(&c->queue, sizeof(unsigned long long));
+    }
     if (e != cudaSuccess) {
-        delete c;
+        ga_destroy(c);
         return (int)e;
     }
     *out = c;
@@ -187,8 +211,7 @@ void ga_destroy(ga_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (Slot& sl : c->slot) sl.release();
-    if (c->overflow) cudaFree(c->overflow);
-    if (c->queue) cudaFree(c->queue);
+    c->scratch.release();
     for (cudaStream_t s : {c->stream, c->stream_in, c->stream_out})
         if (s) cudaStreamDestroy(s);
     delete c;
@@ -212,19 +235,12 @@ static uint32_t pack_priority(const char* pr) {
     return v;
 }
 
-int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
-                          ga_batch_out* out, void* stream_ptr) {
-    if (!c) return -1;
-    char msg[160];
-    if (ga_check_config(cfg, msg, sizeof msg)) {
-        c->err = msg;
-        return -2;
-    }
-    c->launches = 0;
-    if (in->n_pairs <= 0) return 0;
-    cudaError_t e = cudaSetDevice(c->device);
-    if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
-    cudaStream_t st = stream_ptr ? (cudaStream_t)stream_ptr : c->stream;
+// one fused DC+TB launch over device buffers with the given scratch
+static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
+                        const ga_batch_out* out, cudaStream_t st, Scratch* sc) {
+    cudaError_t e;
+    if (!sc->queue && (e = cudaMalloc(&sc->queue, sizeof(unsigned long long))))
+        return fail(c, e, "cudaMalloc");
     genasm::KernelParams P{};
     P.codes = in->codes;
     P.pat_off = in->pat_off;
@@ -252,17 +268,34 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     P.ops = out->ops;
     P.win_off = out->win_off;
     P.dists = out->window_distances;
-    P.queue = c->queue;
-    e = cudaMemsetAsync(c->queue, 0, sizeof(unsigned long long), st);
+    P.queue = sc->queue;
+    e = cudaMemsetAsync(sc->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
     const int group = env_int("GA_GROUP", 8);
     const int block = env_int("GA_BLOCK", 0);
-    e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &c->overflow,
-                                       &c->overflow_cap, &c->last_shape);
+    e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &sc->overflow,
+                                       &sc->overflow_cap, &c->last_shape);
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
-    c->launches = 1;
     return 0;
+}
+
+int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
+                          ga_batch_out* out, void* stream_ptr) {
+    if (!c) return -1;
+    char msg[160];
+    if (ga_check_config(cfg, msg, sizeof msg)) {
+        c->err = msg;
+        return -2;
+    }
+    c->launches = 0;
+    if (in->n_pairs <= 0) return 0;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
+    cudaStream_t st = stream_ptr ? (cudaStream_t)stream_ptr : c->stream;
+    const int rc = launch_batch(c, in, cfg, out, st, &c->scratch);
+    if (rc == 0) c->launches = 1;
+    return rc;
 }
 
 int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out) {
@@ -285,13 +318,12 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
 
-    // ---- chunk plan: consecutive pairs; 2 chunks overlap copies with the kernel
-    // when the batch is large enough that each chunk still fills the GPU ----
-    int chunks = env_int("GA_CHUNKS", n >= 65536 ? 2 : 1);
+    // ---- chunk plan: consecutive pairs, pipelined over kSlots slots.  Chunking
+    // needs output offsets that grow with the input index (the prefix-sum
+    // layout every caller in this package uses); otherwise one chunk. ----
+    int chunks = env_int("GA_CHUNKS", (int)std::min<int64_t>(6, std::max<int64_t>(1, n / 12000)));
     if (chunks < 1) chunks = 1;
     if (chunks > n) chunks = (int)n;
-    // chunking needs output offsets that grow with the input index (the
-    // prefix-sum layout every caller in this package uses)
     for (int64_t q = 1; q < n && chunks > 1; ++q)
         if (out->ops_off[q] < out->ops_off[q - 1] || out->win_off[q] < out->win_off[q - 1])
             chunks = 1;
@@ -299,60 +331,64 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     for (int k = 0; k < chunks; ++k) {
         const int64_t q0 = n * k / chunks, q1 = n * (k + 1) / chunks;
         const int64_t m = q1 - q0;
-        Slot& S = c->slot[k & 1];
-        // the symbol, op and window ranges the chunk touches
+        Slot& S = c->slot[k % kSlots];
+        // the symbol range the chunk reads
         int64_t lo = INT64_MAX, hi = 0;
         for (int64_t q = q0; q < q1; ++q) {
             lo = std::min(lo, std::min(in->pat_off[q], in->txt_off[q]));
             hi = std::max(hi, std::max(in->pat_off[q] + in->pat_len[q], in->txt_off[q] + in->txt_len[q]));
         }
         if (lo > hi) lo = hi;
-        int64_t olo = INT64_MAX, ohi = 0, wlo = INT64_MAX, whi = 0;
-        for (int64_t q = q0; q < q1; ++q) {
-            olo = std::min(olo, out->ops_off[q]);
-            wlo = std::min(wlo, out->win_off[q]);
-        }
-        // a pair's capacity ends where the next larger offset (or the buffer) begins
-        ohi = out->ops_capacity;
-        whi = out->win_capacity;
-        for (int64_t q = 0; q < n; ++q) {
-            if (q >= q0 && q < q1) continue;
-            if (out->ops_off[q] >= olo) ohi = std::min(ohi, out->ops_off[q]);
-            if (out->win_off[q] >= wlo) whi = std::min(whi, out->win_off[q]);
+        // the op and window ranges it writes: up to the next chunk's first pair
+        int64_t olo, ohi, wlo, whi;
+        if (chunks == 1) {
+            olo = *std::min_element(out->ops_off, out->ops_off + n);
+            wlo = *std::min_element(out->win_off, out->win_off + n);
+            ohi = out->ops_capacity;
+            whi = out->win_capacity;
+        } else {
+            olo = out->ops_off[q0];
+            wlo = out->win_off[q0];
+            ohi = q1 < n ? out->ops_off[q1] : out->ops_capacity;
+            whi = q1 < n ? out->win_off[q1] : out->win_capacity;
         }
         const int64_t base = in->packed2 ? (lo & ~int64_t(3)) : lo;
         const int64_t nsym = hi - base;
-        // chunk-local host arrays (rebased offsets, LPT order)
-        S.h_pat_off.resize((size_t)m);
-        S.h_txt_off.resize((size_t)m);
-        S.h_ops_off.resize((size_t)m);
-        S.h_win_off.resize((size_t)m);
-        S.h_order.resize((size_t)m);
-        for (int64_t q = 0; q < m; ++q) {
-            S.h_pat_off[(size_t)q] = in->pat_off[q0 + q] - base;
-            S.h_txt_off[(size_t)q] = in->txt_off[q0 + q] - base;
-            S.h_ops_off[(size_t)q] = out->ops_off[q0 + q] - olo;
-            S.h_win_off[(size_t)q] = out->win_off[q0 + q] - wlo;
-        }
-        if (in->order && chunks == 1) {
-            std::copy(in->order, in->order + n, S.h_order.begin());
-        } else {
-            ga_lpt_order(m, in->pat_len + q0, S.h_order.data());
-        }
-        int64_t nexc = 0, exc0 = 0;
-        if (in->packed2 && in->n_exceptions > 0) {
-            exc0 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions, base) -
-                   in->exceptions;
-            const int64_t exc1 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions,
-                                                  hi) - in->exceptions;
-            nexc = exc1 - exc0;
-        }
         const int64_t nops = ohi - olo;
         const int64_t nwin = whi - wlo;
-        if ((e = S.codes.ensure((size_t)nsym + 16)) || (e = S.pat_off.ensure((size_t)m * 8)) ||
-            (e = S.txt_off.ensure((size_t)m * 8)) || (e = S.pat_len.ensure((size_t)m * 4)) ||
-            (e = S.txt_len.ensure((size_t)m * 4)) || (e = S.order.ensure((size_t)m * 4)) ||
-            (e = S.ops_off.ensure((size_t)m * 8)) || (e = S.win_off.ensure((size_t)m * 8)) ||
+        int64_t nexc = 0, exc0 = 0;
+        if (in->packed2 && in->n_exceptions > 0) {
+            const int64_t* x0 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions, base);
+            const int64_t* x1 = std::lower_bound(x0, in->exceptions + in->n_exceptions, hi);
+            exc0 = x0 - in->exceptions;
+            nexc = x1 - x0;
+        }
+
+        // ---- the slot is free once its previous chunk's copies are done ----
+        if (S.used && (e = cudaEventSynchronize(S.in_done))) return fail(c, e, "slot wait");
+        const size_t meta_bytes = (size_t)m * 44;
+        if (meta_bytes > S.h_meta_cap) {
+            if (S.h_meta) cudaFreeHost(S.h_meta);
+            S.h_meta = nullptr;
+            S.h_meta_cap = 0;
+            if ((e = cudaHostAlloc(&S.h_meta, meta_bytes, cudaHostAllocDefault)))
+                return fail(c, e, "cudaHostAlloc");
+            S.h_meta_cap = meta_bytes;
+        }
+        int64_t* h64 = (int64_t*)S.h_meta;
+        int32_t* h32 = (int32_t*)(h64 + 4 * m);
+        for (int64_t q = 0; q < m; ++q) {
+            h64[q] = in->pat_off[q0 + q] - base;
+            h64[m + q] = in->txt_off[q0 + q] - base;
+            h64[2 * m + q] = out->ops_off[q0 + q] - olo;
+            h64[3 * m + q] = out->win_off[q0 + q] - wlo;
+        }
+        memcpy(h32, in->pat_len + q0, (size_t)m * 4);
+        memcpy(h32 + m, in->txt_len + q0, (size_t)m * 4);
+        if (in->order && chunks == 1) memcpy(h32 + 2 * m, in->order, (size_t)m * 4);
+        else ga_lpt_order(m, in->pat_len + q0, h32 + 2 * m);
+
+        if ((e = S.codes.ensure((size_t)nsym + 16)) || (e = S.meta.ensure(meta_bytes)) ||
             (e = S.results.ensure((size_t)m * sizeof(ga_pair_result))) ||
             (e = S.ops.ensure((size_t)nops + 16)) || (e = S.dists.ensure((size_t)nwin + 16)))
             return fail(c, e, "cudaMalloc");
@@ -362,29 +398,26 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
         if (out->ops2 && (e = S.ops2.ensure((size_t)(nops + 3) / 4 + 16)))
             return fail(c, e, "cudaMalloc");
 
-        // ---- H2D (input stream), after this slot's previous chunk left the device ----
-        cudaStream_t si = c->stream_in, sk = c->stream, so = c->stream_out;
-        if (k >= 2 && (e = cudaStreamWaitEvent(si, S.out_done, 0))) return fail(c, e, "wait");
+        // ---- H2D on the input stream, after the slot's previous chunk left the device ----
+        cudaStream_t si = c->stream_in, sk = S.stream, so = c->stream_out;
+        if (S.used && (e = cudaStreamWaitEvent(si, S.out_done, 0))) return fail(c, e, "wait");
         auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
             return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, si) : cudaSuccess;
         };
-        if (in->packed2) {
-            e = h2d(S.packed.ptr, in->codes + base / 4, (size_t)(nsym + 3) / 4);
-            if (!e && nexc) e = h2d(S.exc.ptr, in->exceptions + exc0, (size_t)nexc * 8);
-        } else {
-            e = h2d(S.codes.ptr, in->codes + base, (size_t)nsym);
+        e = h2d(S.meta.ptr, S.h_meta, meta_bytes);
+        if (!e) {
+            if (in->packed2) {
+                e = h2d(S.packed.ptr, in->codes + base / 4, (size_t)(nsym + 3) / 4);
+                if (!e && nexc) e = h2d(S.exc.ptr, in->exceptions + exc0, (size_t)nexc * 8);
+            } else {
+                e = h2d(S.codes.ptr, in->codes + base, (size_t)nsym);
+            }
         }
-        if (!e) e = h2d(S.pat_off.ptr, S.h_pat_off.data(), (size_t)m * 8);
-        if (!e) e = h2d(S.txt_off.ptr, S.h_txt_off.data(), (size_t)m * 8);
-        if (!e) e = h2d(S.pat_len.ptr, in->pat_len + q0, (size_t)m * 4);
-        if (!e) e = h2d(S.txt_len.ptr, in->txt_len + q0, (size_t)m * 4);
-        if (!e) e = h2d(S.order.ptr, S.h_order.data(), (size_t)m * 4);
-        if (!e) e = h2d(S.ops_off.ptr, S.h_ops_off.data(), (size_t)m * 8);
-        if (!e) e = h2d(S.win_off.ptr, S.h_win_off.data(), (size_t)m * 8);
         if (!e) e = cudaEventRecord(S.in_done, si);
         if (e) return fail(c, e, "H2D copy");
+        S.used = true;
 
-        // ---- compute stream: expand 2-bit sequences, align, pack ops ----
+        // ---- the slot's kernel stream: expand 2-bit sequences, align, pack ops ----
         if ((e = cudaStreamWaitEvent(sk, S.in_done, 0))) return fail(c, e, "wait");
         if (in->packed2) {
             if ((e = genasm::launch_unpack2((const uint8_t*)S.packed.ptr, nsym, (uint8_t*)S.codes.ptr,
@@ -394,26 +427,28 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
                 return fail(c, e, "unpack kernel");
             launches += 1 + (nexc > 0);
         }
+        const int64_t* d64 = (const int64_t*)S.meta.ptr;
+        const int32_t* d32 = (const int32_t*)(d64 + 4 * m);
         ga_batch_in din{};
         din.n_pairs = m;
         din.codes = (const uint8_t*)S.codes.ptr;
         din.codes_len = nsym;
-        din.pat_off = (const int64_t*)S.pat_off.ptr;
-        din.pat_len = (const int32_t*)S.pat_len.ptr;
-        din.txt_off = (const int64_t*)S.txt_off.ptr;
-        din.txt_len = (const int32_t*)S.txt_len.ptr;
-        din.order = (const int32_t*)S.order.ptr;
+        din.pat_off = d64;
+        din.txt_off = d64 + m;
+        din.pat_len = d32;
+        din.txt_len = d32 + m;
+        din.order = d32 + 2 * m;
         ga_batch_out dout{};
         dout.results = (ga_pair_result*)S.results.ptr;
-        dout.ops_off = (const int64_t*)S.ops_off.ptr;
+        dout.ops_off = d64 + 2 * m;
         dout.ops = (uint8_t*)S.ops.ptr;
         dout.ops_capacity = nops;
-        dout.win_off = (const int64_t*)S.win_off.ptr;
+        dout.win_off = d64 + 3 * m;
         dout.window_distances = (uint8_t*)S.dists.ptr;
         dout.win_capacity = nwin;
-        int rc = ga_align_batch_device(c, &din, cfg, &dout, sk);
+        const int rc = launch_batch(c, &din, cfg, &dout, sk, &S.scratch);
         if (rc) return rc;
-        launches += c->launches;
+        launches += 1;
         if (out->ops2) {
             if ((e = genasm::launch_pack_ops((const uint8_t*)S.ops.ptr, nops, (uint8_t*)S.ops2.ptr, sk)))
                 return fail(c, e, "pack kernel");
@@ -421,7 +456,7 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
         }
         if ((e = cudaEventRecord(S.kern_done, sk))) return fail(c, e, "record");
 
-        // ---- D2H (output stream) ----
+        // ---- D2H on the output stream ----
         if ((e = cudaStreamWaitEvent(so, S.kern_done, 0))) return fail(c, e, "wait");
         auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
             return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, so) : cudaSuccess;

@@ -56,7 +56,13 @@ genasm_kernel(const KernelParams P) {
     // per-pair accumulators (meaningful in lane q == 0)
     int64_t cost = 0, rows = 0, reads = 0, writes = 0, words = 0;
 
+    // called by all G lanes of the group
     auto write_result = [&](int status, int fail_window) {
+        if (status == 1 || status == 3) {  // windows the pair never completed read as 0
+            const int64_t step = W - O;
+            const int64_t nwin = Lp <= W ? 1 : 1 + (Lp - W + step - 1) / step;
+            for (int64_t i = fail_window + q; i < nwin; i += G) dists[i] = 0;
+        }
         if (q == 0) {
             PairResult r{};
             r.status = status;
