@@ -272,10 +272,19 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     e = cudaMemsetAsync(sc->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
-    const int group = env_int("GA_GROUP", 8);
-    const int block = env_int("GA_BLOCK", 0);
-    e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &sc->overflow,
-                                       &sc->overflow_cap, &c->last_shape);
+    // GA_KERNEL=thread selects the lane-per-pair kernel (W <= 64); the
+    // lane-group kernel serves everything else
+    const char* kern = getenv("GA_KERNEL");
+    const bool lockstep = P.W > 64 || !(kern && strcmp(kern, "thread") == 0);
+    if (lockstep) {
+        const int group = env_int("GA_GROUP", 8);
+        const int block = env_int("GA_BLOCK", 0);
+        e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &sc->overflow,
+                                           &sc->overflow_cap, &c->last_shape);
+    } else {
+        e = genasm::launch_genasm_thread(P, c->num_sms, st, &sc->overflow, &sc->overflow_cap,
+                                         &c->last_shape);
+    }
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     return 0;
 }

@@ -82,4 +82,8 @@ cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_t
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,
                                    size_t* cap, LaunchShape* shape);
 
+// the lane-per-pair kernel (genasm_thread.cu), W <= 64
+cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_t stream,
+                                 uint32_t** scratch, size_t* cap, LaunchShape* shape);
+
 }  // namespace genasm

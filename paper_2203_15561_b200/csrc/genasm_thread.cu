@@ -1,0 +1,365 @@
+// genasm_thread.cu -- lane-per-pair fused DC+TB kernel (sm_100a), W <= 64.
+//
+// Every lane owns one pair and walks its window chain (window.py:95-120)
+// alone: DC in 32-bit diagonal bands (16 levels, exact for d_min <= 15; see
+// genasm_thread.cuh), traceback from the lane's own band table, next window.
+// No shuffles or cross-lane waits on the hot loop: four 32-bit operations
+// per DC entry.
+//
+// Windows with d_min > 15 (a few percent at 10 % divergence) need the full
+// tier (full-width rows, 16-level passes).  A lane that meets one parks the
+// pair (state saved in its result record, id pushed on the warp's HARD stack
+// in shared memory) and takes another pair, so the warp's fast loop never
+// diverges into the slow path.  When 32 hard windows are parked (or nothing
+// else is left) the warp runs them together: active pairs are parked on the
+// RESUME stack, each lane runs one hard window, the pairs go back on RESUME,
+// and free lanes refill from RESUME before taking fresh pairs from the global
+// queue (longest first).
+//
+// Tables.  Band tier: per warp, [column][word quad][lane] x 16 B -- each
+// column's 16 levels are 8 paired words (genasm_thread.cuh), two coalesced
+// 16-byte stores per lane.  Full tier: per lane,
+// [level][column] x 8 B.  Both live in the context's scratch slab.
+#include "genasm_device.cuh"
+#include "genasm_thread.cuh"
+
+namespace genasm {
+
+namespace {
+
+constexpr int kTBlock = 128;           // threads per block
+constexpr int kWarps = kTBlock / 32;
+constexpr int kStack = 128;            // per-warp HARD / RESUME stack entries
+constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
+
+struct BandTab {
+    uint4* base;  // this warp's region: [column][word quad][lane] x 16 B
+    int lane;
+    __device__ __forceinline__ void put(int j, const uint32_t* w) {
+        uint4* p = base + (size_t)(j - 1) * 64 + lane;
+        p[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        p[32] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+    __device__ __forceinline__ uint32_t get(int k, int c) const {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(base + (size_t)(c - 1) * 64 +
+                                                              (k >> 2) * 32 + lane);
+        return p[k & 3];
+    }
+};
+
+struct FullTab {
+    uint64_t* base;  // this lane's rows, [level][column 1..W]
+    int W;
+    __device__ __forceinline__ void put(int d, int j, uint64_t v) {
+        base[(size_t)d * W + (j - 1)] = v;
+    }
+    __device__ __forceinline__ uint64_t get(int d, int j) const {
+        return base[(size_t)d * W + (j - 1)];
+    }
+};
+
+// per-lane pair state (between windows)
+struct Lane {
+    int pair;  // -1: none
+    int Lp, Lt, widx;
+    int64_t pat, txt, ops, dst;  // offsets
+    int64_t t, nops, cost, rows, reads, writes, words;
+};
+
+__device__ __forceinline__ void open_pair(const KernelParams& P, Lane& L, int pair) {
+    L.pair = pair;
+    L.Lp = P.pat_len[pair];
+    L.Lt = P.txt_len[pair];
+    L.pat = P.pat_off[pair];
+    L.txt = P.txt_off[pair];
+    L.ops = P.ops_off[pair];
+    L.dst = P.win_off[pair];
+}
+
+__device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int pair) {
+    open_pair(P, L, pair);
+    L.widx = 0;
+    L.t = L.nops = L.cost = L.rows = L.reads = L.writes = L.words = 0;
+}
+
+// park: the running state goes into the pair's own result record
+__device__ __forceinline__ void park(const KernelParams& P, const Lane& L) {
+    PairResult* r = reinterpret_cast<PairResult*>(P.results) + L.pair;
+    r->status = -1;
+    r->fail_window = L.widx;
+    r->cost = L.cost;
+    r->text_consumed = L.t;
+    r->rows_computed = L.rows;
+    r->ops_len = L.nops;
+    r->entry_reads = L.reads;
+    r->entry_writes = L.writes;
+    r->words_allocated = L.words;
+}
+
+__device__ __forceinline__ void unpark(const KernelParams& P, Lane& L, int pair) {
+    open_pair(P, L, pair);
+    const PairResult* r = reinterpret_cast<const PairResult*>(P.results) + pair;
+    L.widx = r->fail_window;
+    L.cost = r->cost;
+    L.t = r->text_consumed;
+    L.rows = r->rows_computed;
+    L.nops = r->ops_len;
+    L.reads = r->entry_reads;
+    L.writes = r->entry_writes;
+    L.words = r->words_allocated;
+}
+
+__device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
+    PairResult r{};
+    r.status = status;
+    r.fail_window = -1;
+    if (status == 0) {
+        r.cost = L.cost;
+        r.text_consumed = L.t;
+        r.rows_computed = L.rows;
+        r.ops_len = L.nops;
+        r.entry_reads = L.reads;
+        r.entry_writes = L.writes;
+        r.words_allocated = L.words;
+    } else if (status != 2) {
+        r.fail_window = L.widx;
+        // windows the pair never completed read as 0
+        const int64_t step = P.W - P.O;
+        const int64_t nwin = L.Lp <= P.W ? 1 : 1 + (L.Lp - P.W + step - 1) / step;
+        for (int64_t i = L.widx; i < nwin; ++i) P.dists[L.dst + i] = 0;
+    }
+    reinterpret_cast<PairResult*>(P.results)[L.pair] = r;
+    L.pair = -1;
+}
+
+enum : int { WIN_NEXT = 0, WIN_HARD = 1 };
+
+// One window of lane L's pair.  FULL = false: band tier, returns WIN_HARD if
+// d_min > 15 (and k allows more); FULL = true: full tier.  On completion of
+// the pair (or failure) the result is written and L.pair = -1.
+template <bool FULL>
+__device__ __forceinline__ int run_window(const KernelParams& P, Lane& L, BandTab& bt, FullTab& ft) {
+    using namespace thr;
+    const int W = P.W, K = P.k;
+    const int64_t p = (int64_t)L.widx * (W - P.O);  // every earlier window consumed W-O
+    const int64_t rem = L.Lp - p;
+    const bool fin = rem <= W;
+    const int m = fin ? (int)rem : W;
+    const int64_t tl = L.Lt - L.t;
+    const int n = tl < W ? (int)(tl > 0 ? tl : 0) : W;
+    const int budget = fin ? m : W - P.O;
+    const Planes pp = load_planes(P.codes + L.pat + p, m);
+    Planes tp{0ull, 0ull, 0ull};
+    int d_min;
+    uint8_t* ops = P.ops + L.ops;
+    TbOut o;
+    bool ok;
+    if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
+        if (m > K) {
+            finish(P, L, 1);
+            return WIN_NEXT;
+        }
+        d_min = m;
+        ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, m, n, d_min, budget,
+                       P.prio_lut, ops, L.nops, o);
+    } else {
+        tp = load_planes(P.codes + L.txt + L.t, n);
+        if (!FULL) {
+            uint32_t okm = dc_band(pp, tp, m, n, bt);
+            const int lim = K < 15 ? K : 15;
+            okm &= (2u << lim) - 1u;
+            if (!okm) {
+                if (K <= 15) {
+                    finish(P, L, 1);
+                    return WIN_NEXT;
+                }
+                return WIN_HARD;
+            }
+            d_min = __ffs(okm) - 1;
+            ok = tb_band(bt, pp, tp, m, n, d_min, budget, P.prio_lut, ops, L.nops, o);
+        } else {
+            d_min = dc_full(pp, tp, m, n, K, ft);
+            if (d_min < 0) {
+                finish(P, L, 1);
+                return WIN_NEXT;
+            }
+            ok = traceback([&](int e, int c, int x) { return full_bit(ft, e, c, x); }, pp, tp, m, n,
+                           d_min, budget, P.prio_lut, ops, L.nops, o);
+        }
+    }
+    if (!ok) {
+        finish(P, L, 3);
+        return WIN_NEXT;
+    }
+    const int64_t wr = window_writes(n, budget, K, d_min);
+    P.dists[L.dst + L.widx] = (uint8_t)d_min;
+    L.rows += d_min + 1;
+    L.cost += o.wcost;
+    L.reads += o.reads;
+    L.writes += wr;
+    L.words += wr * ((m + 63) / 64);
+    L.t += o.tcons;
+    ++L.widx;
+    if (p + o.consumed >= L.Lp) finish(P, L, 0);
+    return WIN_NEXT;
+}
+
+// One full-tier window of a parked pair.  Returns true if the pair goes back
+// on RESUME.
+__device__ __forceinline__ bool hard_window(const KernelParams& P, int pair, uint4* band, int lane,
+                                         uint64_t* full) {
+    Lane L;
+    unpark(P, L, pair);
+    BandTab bt{band, lane};
+    FullTab ft{full, P.W};
+    run_window<true>(P, L, bt, ft);
+    if (L.pair < 0) return false;
+    park(P, L);
+    return true;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kTBlock)
+genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_base,
+                     int64_t full_words_per_lane) {
+    __shared__ int s_hard[kWarps][kStack], s_res[kWarps][kStack];
+    __shared__ int s_nh[kWarps], s_nr[kWarps];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    BandTab bt{reinterpret_cast<uint4*>(band_base + gw * kBandWordsPerWarp), lane};
+    FullTab ft{full_base + (gw * 32 + lane) * full_words_per_lane, P.W};
+    int* hard = s_hard[wib];
+    int* res = s_res[wib];
+    if (lane == 0) s_nh[wib] = s_nr[wib] = 0;
+    __syncwarp();
+    const unsigned lt = lanemask_lt();
+    bool exhausted = false;
+    Lane L;
+    L.pair = -1;
+    for (;;) {
+        // ---- free lanes take parked pairs first, then fresh ones (longest first) ----
+        unsigned freem = __ballot_sync(FULL, L.pair < 0);
+        if (freem) {
+            const int nr = s_nr[wib];
+            const int rank = __popc(freem & lt);
+            const int take = min(__popc(freem), nr);
+            if (L.pair < 0 && rank < take) unpark(P, L, res[nr - 1 - rank]);
+            __syncwarp();
+            if (lane == 0) s_nr[wib] = nr - take;
+            freem = __ballot_sync(FULL, L.pair < 0);
+            if (freem && !exhausted) {
+                const int cnt = __popc(freem);
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(P.queue, (unsigned long long)cnt);
+                base = __shfl_sync(FULL, base, 0);
+                if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
+                if (L.pair < 0) {
+                    const unsigned long long idx = base + __popc(freem & lt);
+                    if (idx < (unsigned long long)P.n_pairs) {
+                        const int pair = P.order ? P.order[idx] : (int)idx;
+                        fresh_pair(P, L, pair);
+                        if (L.Lp <= 0) finish(P, L, 2);  // EmptyPattern (window.py:87-88)
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int nh = s_nh[wib];
+        const unsigned active = __ballot_sync(FULL, L.pair >= 0);
+        if (!active && nh == 0 && s_nr[wib] == 0 && exhausted) break;
+
+        // parked hard windows run as a batch once 32 wait, or once at least
+        // half of the warp's pairs in flight are parked (lanes would idle)
+        const int nact = __popc(active);
+        if (nh >= 32 || (nh > 0 && nh >= nact + s_nr[wib])) {
+            // ---- hard batch: park the active pairs, run up to 32 full-tier windows ----
+            int nr = s_nr[wib];
+            if (L.pair >= 0) {
+                park(P, L);
+                res[nr + __popc(active & lt)] = L.pair;
+                L.pair = -1;
+            }
+            nr += __popc(active);
+            const int take = nh < 32 ? nh : 32;
+            int hp = -1;
+            if (lane < take) {
+                hp = hard[nh - 1 - lane];
+                if (!hard_window(P, hp, bt.base, lane, ft.base)) hp = -1;
+            }
+            const unsigned back = __ballot_sync(FULL, hp >= 0);
+            if (hp >= 0) res[nr + __popc(back & lt)] = hp;
+            __syncwarp();
+            if (lane == 0) {
+                s_nr[wib] = nr + __popc(back);
+                s_nh[wib] = nh - take;
+            }
+            __syncwarp();
+            continue;
+        }
+        if (!active) continue;
+
+        // ---- one band-tier window per active lane ----
+        int r = WIN_NEXT;
+        if (L.pair >= 0) r = run_window<false>(P, L, bt, ft);
+        const unsigned hm = __ballot_sync(FULL, r == WIN_HARD);
+        if (hm) {
+            if (r == WIN_HARD) {
+                park(P, L);
+                hard[nh + __popc(hm & lt)] = L.pair;
+                L.pair = -1;
+            }
+            __syncwarp();
+            if (lane == 0) s_nh[wib] = nh + __popc(hm);
+            __syncwarp();
+        }
+    }
+}
+
+cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_t stream,
+                                 uint32_t** scratch, size_t* cap, LaunchShape* shape) {
+    if (P.W > 64) return cudaErrorInvalidValue;
+    int per_sm = 0;
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, genasm_thread_kernel, kTBlock, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const char* cap_env = getenv("GA_WARPS_PER_SM");
+    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 16;
+    const int bcap = warps_cap / kWarps;
+    if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
+    int grid = num_sms * per_sm;
+    const int64_t max_useful = (P.n_pairs + kTBlock - 1) / kTBlock;
+    if (grid > max_useful) grid = (int)(max_useful > 0 ? max_useful : 1);
+    // full-tier rows: levels 0..k (+ a pass of slack) x W columns x 8 bytes per lane
+    const int64_t full_words = (int64_t)(P.k + 1) * P.W * 2;
+    const size_t warps = (size_t)grid * kWarps;
+    const size_t band_words = warps * kBandWordsPerWarp;
+    const size_t need = band_words + warps * 32 * (size_t)full_words + 64;
+    if (need > *cap || !*scratch) {
+        if (*scratch) cudaFree(*scratch);
+        *scratch = nullptr;
+        *cap = 0;
+        e = cudaMalloc(scratch, need * 4);
+        if (e != cudaSuccess) return e;
+        *cap = need;
+    }
+    uint32_t* band = *scratch;
+    uint64_t* full = reinterpret_cast<uint64_t*>(*scratch + ((band_words + 63) & ~(size_t)63));
+    genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, full, full_words / 2);
+    shape->grid = grid;
+    shape->block = kTBlock;
+    shape->smem_bytes = 0;
+    shape->group = 1;
+    shape->blocks_per_sm = per_sm;
+    shape->overflow_words_per_group = full_words;
+    return cudaGetLastError();
+}
+
+}  // namespace genasm

@@ -1,0 +1,482 @@
+// genasm_thread.cuh -- one window of improved GenASM (DC + TB) computed by ONE
+// thread: the building blocks of the lane-per-pair kernel (genasm_thread.cu).
+// Host + device code, so tools/thread_model.cpp can check it against the
+// oracle on the CPU.
+//
+// Reference algorithm (0 = active):
+//   R[d][0] = init(m, d)              bits < min(d, m) zero  (bitvec.py:108-122)
+//   R[0][j] = sh(R[0][j-1]) | PM[T[j-1]]                      (distance.py:125-133)
+//   R[d][j] = (sh(R[d][j-1]) | PM) & sh(R[d-1][j-1] & R[d-1][j]) & R[d-1][j-1]
+//                                                               (distance.py:134-149)
+// with sh(x) = x << 1 shifting in an active 0, cp / ct the reversed chunks
+// (window.py:99-100) and success at bit m-1 of R[d][n].
+//
+// Diagonal band (fast tier, d_min <= 15).  Cell (i, j) lies on diagonal
+// offset delta = (m-1-i) - (n-j).  An active cell at |delta'| >= 16 can only
+// reach offset delta by |delta'| - |delta| insertion/deletion edges, each one
+// level up, so it can influence level d only if |delta| >= 16 - d.  Every
+// cell the traceback reads from a window with d_min <= 15 has
+// |delta| <= d_min - d <= 15 - d (and its predecessors at level d-1 have
+// |delta +- 1| <= 15 - (d-1)), and the success cell has delta = 0: all are
+// exact when each row is kept only on the 32 diagonals delta in [-16, 15],
+// everything outside treated as inactive.  Column j keeps absolute bits
+// [org_j, org_j + 31] with org_j = max(o_j, 0), o_j = m - n + j - 16.  Moving
+// one column right the band moves up one bit, so in band coordinates
+//   M: sh(R[d][j-1])   -> R[d][j-1] unchanged      S: sh(R[d-1][j-1]) -> a
+//   I: sh(R[d-1][j])   -> (b << 1) | 1            D: R[d-1][j-1]     -> (a >> 1) | 2^31
+// (a = R[d-1][j-1], b = R[d-1][j]; the filled bits are out-of-band cells).
+// While o_j <= 0 the band is pinned at bit 0 and the plain recurrence
+// applies.  Four 32-bit operations per entry instead of 5 * ceil(m/32).
+//
+// Full tier (d_min > 15): full-width 64-bit rows, 4 levels per pass, rows
+// kept in a per-lane table for the traceback.
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define GA_HD __host__ __device__ __forceinline__
+#else
+#define GA_HD inline
+#endif
+
+namespace genasm {
+namespace thr {
+
+constexpr int kFastLevels = 16;   // levels of the band tier (d_min <= 15)
+constexpr int kPassLevels = 4;    // levels per pass of the full tier
+
+enum : int { OPC_M = 0, OPC_S = 1, OPC_I = 2, OPC_D = 3, OPC_STUCK = 5 };
+
+// 2-bit planes of up to 64 symbols, REVERSED: bit x describes src[len-1-x].
+// b0/b1 = bits 0/1 of the code, bn = code 4 (no mask: never matches).
+struct Planes {
+    uint64_t b0, b1, bn;
+};
+
+GA_HD uint64_t brev64(uint64_t x) {
+#ifdef __CUDA_ARCH__
+    return __brevll(x);
+#else
+    x = ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+    x = ((x >> 2) & 0x3333333333333333ull) | ((x & 0x3333333333333333ull) << 2);
+    x = ((x >> 4) & 0x0F0F0F0F0F0F0F0Full) | ((x & 0x0F0F0F0F0F0F0F0Full) << 4);
+    x = ((x >> 8) & 0x00FF00FF00FF00FFull) | ((x & 0x00FF00FF00FF00FFull) << 8);
+    x = ((x >> 16) & 0x0000FFFF0000FFFFull) | ((x & 0x0000FFFF0000FFFFull) << 16);
+    return (x >> 32) | (x << 32);
+#endif
+}
+
+// four code bytes -> the nibble of one bit plane (byte k -> bit k)
+GA_HD uint32_t nib(uint32_t w, int bit) {
+    return (((w >> bit) & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// planes of src[0..len), 1 <= len <= 64, reversed
+GA_HD Planes load_planes(const uint8_t* src, int len) {
+    uint64_t f0 = 0, f1 = 0, fn = 0;
+#ifdef __CUDA_ARCH__
+    // aligned 4-byte words covering [src, src+len); a word never crosses the
+    // allocation because allocations are at least 4-byte granular
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const int sh = (int)(a & 3);  // bytes of the first word before src
+    const int nw = (sh + len + 3) >> 2;
+    for (int k = 0; k < nw; ++k) {
+        const uint32_t w = __ldg(wp + k);
+        const int pos = 4 * k - sh;  // symbol index of the word's byte 0
+        const uint64_t n0 = nib(w, 0), n1 = nib(w, 1), nn = nib(w, 2);
+        if (pos >= 0) {
+            f0 |= n0 << pos;
+            f1 |= n1 << pos;
+            fn |= nn << pos;
+        } else {
+            f0 |= n0 >> -pos;
+            f1 |= n1 >> -pos;
+            fn |= nn >> -pos;
+        }
+    }
+#else
+    for (int k = 0; k < len; ++k) {
+        f0 |= (uint64_t)(src[k] & 1) << k;
+        f1 |= (uint64_t)((src[k] >> 1) & 1) << k;
+        fn |= (uint64_t)((src[k] >> 2) & 1) << k;
+    }
+#endif
+    const int s = 64 - len;  // reverse the first len bits
+    Planes p;
+    p.b0 = brev64(f0) >> s;
+    p.b1 = brev64(f1) >> s;
+    p.bn = brev64(fn) >> s;
+    return p;
+}
+
+GA_HD uint32_t bit64(uint64_t x, int k) { return (uint32_t)(x >> k) & 1u; }
+
+// all-ones iff bit k of x
+GA_HD uint32_t bcast(uint64_t x, int k) { return 0u - (uint32_t)((x >> k) & 1u); }
+
+// init(m, d) restricted to the band at origin org: band bit b is absolute org+b
+GA_HD uint32_t init_band(int m, int d, int org) {
+    const int z = (d < m ? d : m) - org;  // zero below band bit z
+    if (z <= 0) return 0xffffffffu;
+    if (z >= 32) return 0u;
+    return ~((1u << z) - 1u);
+}
+
+GA_HD uint64_t init_row64(int m, int d) {
+    const int z = d < m ? d : m;
+    return z >= 64 ? 0ull : ~((1ull << z) - 1ull);
+}
+
+// three-input logic ops that must stay single instructions
+GA_HD uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+#else
+    return a & b & c;
+#endif
+}
+// (a | b) & c
+GA_HD uint32_t orand(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xA8;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+#else
+    return (a | b) & c;
+#endif
+}
+// (a >> 1) | 2^31 -- the D edge in band coordinates
+GA_HD uint32_t shr1_fill(uint32_t a) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(a, 1u, 1);
+#else
+    return (a >> 1) | 0x80000000u;
+#endif
+}
+// bit `pos` of w; positions outside [0, 32) read as 1 (inactive)
+GA_HD uint32_t wbit(uint32_t w, int pos) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_rc(w, 0xffffffffu, (unsigned)pos) & 1u;
+#else
+    return ((unsigned)pos < 32u) ? (w >> pos) & 1u : 1u;
+#endif
+}
+
+// mismatch word of text symbol k (bits k of the text planes) against the
+// pattern planes' 32-bit window (p0, p1, pn): bit b = 1 iff they differ
+GA_HD uint32_t pm_word(uint32_t p0, uint32_t p1, uint32_t pn, const Planes& tp, int k) {
+    return (p0 ^ bcast(tp.b0, k)) | (p1 ^ bcast(tp.b1, k)) | pn | bcast(tp.bn, k);
+}
+
+// Level pairing.  Reading level e at a band-tier window touches only the
+// diagonals |delta| <= 15 - e, i.e. band bits [e, 30-e]: 31-2e bits for level
+// e and 2e+1 bits for level 15-e, 32 together.  Rotated by 16, level 15-e's
+// bits [15-e, 15+e] land exactly on the bits level e leaves free, so word k
+// of a stored column holds levels k and 15-k (k = 0..7).  Columns whose band
+// is pinned at bit 0 are first shifted to virtual band coordinates.
+GA_HD uint32_t rot16(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __byte_perm(x, 0, 0x1032);
+#else
+    return (x >> 16) | (x << 16);
+#endif
+}
+GA_HD uint32_t pair_word(uint32_t lo, uint32_t hi, int k) {
+    const uint32_t mk = ((1u << (31 - 2 * k)) - 1u) << k;  // bits [k, 30-k]
+    return (lo & mk) | (rot16(hi) & ~mk);
+}
+template <class Tab>
+GA_HD void put_packed(Tab& tab, int j, const uint32_t* col, int shl) {
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t lo = shl ? (shl < 32 ? col[k] << shl : 0u) : col[k];
+        const uint32_t hi = shl ? (shl < 32 ? col[15 - k] << shl : 0u) : col[15 - k];
+        w[k] = pair_word(lo, hi, k);
+    }
+    tab.put(j, w);
+}
+// stored bit at band position b of level e (0 <= e <= 15) from a column's words
+GA_HD uint32_t packed_bit(uint32_t w_lo_or_hi, int e, int b) {
+    const int pos = e <= 7 ? b : b + 16;
+    return (w_lo_or_hi >> (pos & 31)) & 1u;
+}
+GA_HD int packed_word(int e) { return e <= 7 ? e : 15 - e; }
+
+// Band tier DC over columns 1..n of a window (m, n >= 1).  col[] ends as
+// R[d][n] (band at org_n); tab.put(j, w) receives each column's 8 paired
+// words.  Returns the mask of levels d <= 15 with R[d][n] bit m-1 active.
+template <class Tab>
+GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& tab) {
+    uint32_t col[kFastLevels];
+    const int o0 = m - n - 16;
+    const int org0 = o0 > 0 ? o0 : 0;
+#pragma unroll
+    for (int d = 0; d < kFastLevels; ++d) col[d] = init_band(m, d, org0);
+    const uint32_t p0lo = (uint32_t)pp.b0, p1lo = (uint32_t)pp.b1, pnlo = (uint32_t)pp.bn;
+    // columns whose band is pinned at bit 0 (o_j <= 0): the plain recurrence
+    int jA = -o0;
+    jA = jA < 0 ? 0 : (jA > n ? n : jA);
+    for (int j = 1; j <= jA; ++j) {
+        const uint32_t pm = pm_word(p0lo, p1lo, pnlo, tp, j - 1);
+        uint32_t a = col[0];
+        uint32_t xa = a << 1;
+        uint32_t b = xa | pm;
+        col[0] = b;
+#pragma unroll
+        for (int d = 1; d < kFastLevels; ++d) {
+            const uint32_t c = col[d];
+            const uint32_t x = c << 1;
+            const uint32_t nc = and3(orand(x, pm, xa), b << 1, a);
+            a = c;
+            xa = x;
+            col[d] = nc;
+            b = nc;
+        }
+        put_packed(tab, j, col, -(o0 + j));
+    }
+    // banded columns: origin o_j = o0 + j >= 1; four operations per entry
+#pragma unroll 2
+    for (int j = jA + 1; j <= n; ++j) {
+        const int oj = o0 + j;
+        const uint32_t pm = pm_word((uint32_t)(pp.b0 >> oj), (uint32_t)(pp.b1 >> oj),
+                                    (uint32_t)(pp.bn >> oj), tp, j - 1);
+        uint32_t a = col[0];
+        uint32_t b = a | pm;
+        col[0] = b;
+#pragma unroll
+        for (int d = 1; d < kFastLevels; ++d) {
+            const uint32_t c = col[d];
+            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), 2u * b + 1u);
+            a = c;
+            col[d] = nc;
+            b = nc;
+        }
+        put_packed(tab, j, col, 0);
+    }
+    // success bit m-1 sits at band bit m-1-org_n = min(m-1, 15)
+    const int sb = m - 1 < 15 ? m - 1 : 15;
+    uint32_t ok = 0;
+#pragma unroll
+    for (int d = 0; d < kFastLevels; ++d) ok |= ((~col[d] >> sb) & 1u) << d;
+    return ok;
+}
+
+// Full tier DC: passes of 4 levels over full 64-bit rows, rows stored in
+// `ht` (level-major) for the traceback.  Returns d_min <= K or -1.
+template <class HTab>
+GA_HD int dc_full(const Planes& pp, const Planes& tp, int m, int n, int K, HTab& ht) {
+    uint64_t pmask[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+        pmask[s] = (pp.b0 ^ (0ull - (uint64_t)(s & 1))) | (pp.b1 ^ (0ull - (uint64_t)(s >> 1))) |
+                   pp.bn;
+    const uint64_t tb = 1ull << (m - 1);
+    for (int d0 = 0; d0 <= K; d0 += kPassLevels) {
+        uint64_t col[kPassLevels];
+#pragma unroll
+        for (int k = 0; k < kPassLevels; ++k) col[k] = init_row64(m, d0 + k);
+        uint64_t aprev = d0 > 0 ? init_row64(m, d0 - 1) : 0ull;
+        // rows of level d0-1, loaded two columns ahead
+        uint64_t bl1 = d0 > 0 ? ht.get(d0 - 1, 1) : 0ull;
+        uint64_t bl2 = (d0 > 0 && n >= 2) ? ht.get(d0 - 1, 2) : 0ull;
+        for (int j = 1; j <= n; ++j) {
+            const uint64_t bl = bl1;
+            bl1 = bl2;
+            bl2 = (d0 > 0 && j + 2 <= n) ? ht.get(d0 - 1, j + 2) : 0ull;
+            const int s = (int)(bit64(tp.b0, j - 1) | bit64(tp.b1, j - 1) << 1);
+            const uint64_t pm = bit64(tp.bn, j - 1) ? ~0ull : pmask[s];
+            uint64_t a = aprev, b = bl;
+#pragma unroll
+            for (int k = 0; k < kPassLevels; ++k) {
+                const uint64_t c = col[k];
+                const uint64_t nc = (d0 + k == 0) ? ((c << 1) | pm)
+                                                  : (((c << 1) | pm) & ((a & b) << 1) & a);
+                a = c;
+                b = nc;
+                col[k] = nc;
+                if (d0 + k <= K) ht.put(d0 + k, j, nc);
+            }
+            aprev = bl;
+        }
+#pragma unroll
+        for (int k = 0; k < kPassLevels; ++k)
+            if (d0 + k <= K && !(col[k] & tb)) return d0 + k;
+    }
+    return -1;
+}
+
+template <class HTab>
+GA_HD uint32_t full_bit(HTab& ht, int e, int c, int x) {
+    return (uint32_t)(ht.get(e, c) >> x) & 1u;
+}
+
+// Traceback of one window (backtrace.py:88-160), from (j=n, d=d_min, i=m-1)
+// until the budget is consumed.  BIT(e, c, x) returns table bit x of level e,
+// column c >= 1 (1 = inactive); column 0 is init(m, .) and read analytically.
+// Writes ops (ASCII) at ops[nops..]; returns false if the walk got stuck.
+struct TbOut {
+    int consumed, tcons, wcost;
+    int64_t reads;
+};
+
+template <class BitFn>
+GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int n, int d_min,
+                     int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
+    int d = d_min, j = n, i = m - 1;
+    o.consumed = o.tcons = o.wcost = 0;
+    o.reads = 0;
+    for (;;) {
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+            if (i + 1 > d) return false;
+            const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
+            for (int u = 0; u < take; ++u) ops[nops + u] = 'I';
+            nops += take;
+            o.wcost += take;
+            o.consumed += take;
+            return true;
+        }
+        const bool symeq = !bit64(tp.bn, j - 1) && !bit64(pp.bn, i) &&
+                           bit64(tp.b0, j - 1) == bit64(pp.b0, i) &&
+                           bit64(tp.b1, j - 1) == bit64(pp.b1, i);
+        const int dm1 = d > 0 ? d - 1 : 0;
+        uint32_t mb = 0, sb = 0, db, ib = 0;
+        if (j == 1) {  // column 0 = init(m, .): bit x inactive iff x >= level
+            mb = i - 1 >= d;
+            sb = i - 1 >= d - 1;
+            db = i >= d - 1;
+        } else {
+            if (i >= 1) {
+                mb = BIT(d, j - 1, i - 1);
+                sb = BIT(dm1, j - 1, i - 1);
+            }
+            db = BIT(dm1, j - 1, i);
+        }
+        if (i >= 1) ib = BIT(dm1, j, i - 1);
+        const bool dpos = d > 0;
+        const bool mok = symeq && (i == 0 || !mb);
+        const bool sok = dpos && (i == 0 || !sb);
+        const bool iok = dpos && (i == 0 || !ib);
+        const bool dok = dpos && !db;
+        const unsigned okm =
+            (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+        const int op = (int)((prio_lut >> (4 * okm)) & 0xFu);
+        o.reads += (j >= 2) + (dpos ? (j >= 2) + 1 : 0);
+        if (op == OPC_M) {
+            ops[nops++] = '=';
+            --j; --i; ++o.consumed; ++o.tcons;
+        } else if (op == OPC_S) {
+            ops[nops++] = 'X';
+            --j; --d; --i; ++o.consumed; ++o.tcons; ++o.wcost;
+        } else if (op == OPC_I) {
+            ops[nops++] = 'I';
+            --d; --i; ++o.consumed; ++o.wcost;
+        } else if (op == OPC_D) {
+            ops[nops++] = 'D';
+            --j; --d; ++o.tcons; ++o.wcost;
+        } else {
+            return false;
+        }
+    }
+}
+
+// Traceback of a band-tier window: the walk of traceback() with the level
+// bits read from the paired band words (positions relative to each column's
+// virtual band origin o_j) and the '=' test from the symbol planes.
+template <class Tab>
+GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
+                   int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
+    constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
+    int d = d_min, j = n, i = m - 1;
+    const int o0 = m - n - 16;
+    o.consumed = o.tcons = o.wcost = 0;
+    o.reads = 0;
+    for (;;) {
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+            if (i + 1 > d) return false;
+            const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
+            for (int u = 0; u < take; ++u) ops[nops + u] = 'I';
+            nops += take;
+            o.wcost += take;
+            o.consumed += take;
+            return true;
+        }
+        const int u = i - (o0 + j);  // band position of (i, j); (i-1, j-1) shares it
+        const int dm1 = d > 0 ? d - 1 : 0;
+        const uint32_t wj = tab.get(packed_word(dm1), j);
+        uint32_t mb, sb, db;
+        if (j >= 2) {
+            const uint32_t w1 = tab.get(packed_word(d), j - 1);
+            const uint32_t w2 = tab.get(packed_word(dm1), j - 1);
+            mb = packed_bit(w1, d, u);
+            sb = packed_bit(w2, dm1, u);
+            db = packed_bit(w2, dm1, u + 1);
+        } else {  // column 0 = init(m, .): bit x inactive iff x >= level
+            mb = i - 1 >= d;
+            sb = i - 1 >= d - 1;
+            db = i >= d - 1;
+        }
+        const uint32_t ib = packed_bit(wj, dm1, u - 1);
+        const bool symeq = !bit64(tp.bn, j - 1) && !bit64(pp.bn, i) &&
+                           bit64(tp.b0, j - 1) == bit64(pp.b0, i) &&
+                           bit64(tp.b1, j - 1) == bit64(pp.b1, i);
+        const bool dpos = d > 0;
+        const bool i0 = i == 0;
+        const bool mok = symeq && (i0 || !mb);
+        const bool sok = dpos && (i0 || !sb);
+        const bool iok = dpos && (i0 || !ib);
+        const bool dok = dpos && !db;
+        const unsigned okm =
+            (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+        const int op = (int)((prio_lut >> (4 * okm)) & 0xFu);
+        o.reads += (j >= 2) + (dpos ? (j >= 2) + 1 : 0);
+        if (op > OPC_D) return false;
+        ops[nops++] = (uint8_t)(kChars >> (8 * op));
+        const int mj = op != OPC_I;  // M, S, D consume a text symbol
+        const int mi = op != OPC_D;  // M, S, I consume a pattern symbol
+        const int md = op != OPC_M;
+        j -= mj;
+        i -= mi;
+        d -= md;
+        o.consumed += mi;
+        o.tcons += mj;
+        o.wcost += md;
+    }
+}
+
+// entry_writes of one window in closed form (dptable.py:62-82, 156-171):
+// level d stores columns max(1, n - budget - (K - d) - 1) .. n
+GA_HD int64_t window_writes(int n, int budget, int K, int d_min) {
+    int64_t wr = 0;
+    for (int dd = 0; dd <= d_min; ++dd) {
+        int ss = n - budget - (K - dd) - 1;
+        ss = ss > 1 ? ss : 1;
+        const int cnt = n - ss + 1;
+        wr += cnt > 0 ? cnt : 0;
+    }
+    return wr;
+}
+
+// first active edge in priority order for each 4-bit mask of active edges
+// (backtrace.py:134-160); 5 = none
+GA_HD uint64_t make_prio_lut(const char* prio) {
+    uint64_t lut = 0;
+    for (uint64_t mask = 0; mask < 16; ++mask) {
+        uint64_t op = OPC_STUCK;
+        for (int u = 3; u >= 0; --u) {
+            const char c = prio[u];
+            const uint64_t id = c == 'M' ? 0 : c == 'S' ? 1 : c == 'I' ? 2 : 3;
+            if (mask & (1ull << id)) op = id;
+        }
+        lut |= op << (4 * mask);
+    }
+    return lut;
+}
+
+}  // namespace thr
+}  // namespace genasm

@@ -1,0 +1,62 @@
+"""Device-resident timing of the fused kernel (ncu target; dev tool).
+
+    python tools/dev_kernel.py [config] [count] [reps]
+Runs ga_align_batch_device `reps` times on one config's pairs (inputs already
+in HBM) and prints the CUDA-event time per launch.  Knobs: GA_GROUP,
+GA_BLOCK, GA_WARPS_PER_SM (read by the library at each launch).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2203_15561_b200 import _abi, engine, sim  # noqa: E402
+
+
+def main():
+    cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    count = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else None
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+    batch, _ = sim.config_pairs(cfg_id, count=count)
+    n = batch.n_pairs
+    L = engine.lib()
+    ctx = engine.context(0)
+    cfg = _abi.make_config(64, 24, 64, "MSID")
+    host = _abi.PackedResults.allocate(batch, 64, 24)
+    dev = torch.device("cuda:0")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    order = engine.lpt_order(batch.pat_len)
+    d = [up(x) for x in (batch.codes, batch.pat_off, batch.pat_len, batch.txt_off, batch.txt_len,
+                         order, host.ops_off, host.win_off)]
+    res = torch.empty(n * 64, dtype=torch.uint8, device=dev)
+    ops = torch.empty(host.ops.shape[0], dtype=torch.uint8, device=dev)
+    dst = torch.empty(host.dists.shape[0], dtype=torch.uint8, device=dev)
+    din = _abi.GaBatchIn(n, d[0].data_ptr(), int(batch.codes.shape[0]), d[1].data_ptr(),
+                         d[2].data_ptr(), d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr())
+    dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
+                           d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
+    st = torch.cuda.Stream(dev)
+    times = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        rc = L.ga_align_batch_device(ctx, C.byref(din), C.byref(cfg), C.byref(dout),
+                                     C.c_void_p(st.cuda_stream))
+        b.record(st)
+        assert rc == 0, L.ga_last_error(ctx)
+        st.synchronize()
+        times.append(a.elapsed_time(b))
+    r = res.cpu().numpy().view(_abi.RESULT_DTYPE)
+    print(f"config {cfg_id} n={n} ms/launch {[round(x, 2) for x in times]} "
+          f"best {min(times):.2f} ({n / min(times) * 1e3 / 1e6:.3f} M aln/s) "
+          f"status {np.bincount(r['status'], minlength=4).tolist()}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

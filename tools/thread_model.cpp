@@ -1,0 +1,126 @@
+// thread_model.cpp -- dev tool: the lane-per-pair window code of
+// csrc/genasm_thread.cuh run on the host, one pair at a time, so the band /
+// full-tier math can be checked against the oracle without a GPU.
+//   g++ -O2 -std=c++17 -shared -fPIC -o tools/_thread_model.so tools/thread_model.cpp
+#include <stdint.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../include/genasm.h"
+#include "../paper_2203_15561_b200/csrc/genasm_thread.cuh"
+
+using namespace genasm::thr;
+
+struct HostBand {
+    std::vector<uint32_t> w;  // [column][8 paired words]
+    void reset(int n) { w.assign((size_t)(n + 1) * 8, 0xdeadbeefu); }
+    void put(int j, const uint32_t* pw) { memcpy(&w[(size_t)j * 8], pw, 32); }
+    uint32_t get(int k, int c) const { return w[(size_t)c * 8 + k]; }
+};
+
+struct HostFull {
+    std::vector<uint64_t> w;  // [level][column]
+    int W = 0;
+    void reset(int levels, int W_) {
+        W = W_;
+        w.assign((size_t)levels * (W + 1), 0x5555aaaa5555aaaaull);
+    }
+    void put(int d, int j, uint64_t v) { w[(size_t)d * (W + 1) + j] = v; }
+    uint64_t get(int d, int j) const { return w[(size_t)d * (W + 1) + j]; }
+};
+
+extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out,
+                                 int64_t* tier_counts) {
+    const int W = cfg->window, O = cfg->overlap, K = cfg->k;
+    if (W > 64) return -2;
+    const uint64_t lut = make_prio_lut(cfg->priority);
+    HostBand band;
+    HostFull full;
+    for (int64_t q = 0; q < in->n_pairs; ++q) {
+        ga_pair_result& r = out->results[q];
+        memset(&r, 0, sizeof r);
+        r.fail_window = -1;
+        const int Lp = in->pat_len[q], Lt = in->txt_len[q];
+        const uint8_t* P = in->codes + in->pat_off[q];
+        const uint8_t* T = in->codes + in->txt_off[q];
+        uint8_t* ops = out->ops + out->ops_off[q];
+        uint8_t* dists = out->window_distances + out->win_off[q];
+        if (Lp <= 0) {
+            r.status = GA_EMPTY_PATTERN;
+            continue;
+        }
+        int64_t p = 0, t = 0, nops = 0;
+        int widx = 0;
+        int status = GA_OK;
+        while (p < Lp) {
+            const int64_t rem = Lp - p;
+            const bool fin = rem <= W;
+            const int m = fin ? (int)rem : W;
+            const int64_t tl = Lt - t;
+            const int n = tl < W ? (int)(tl > 0 ? tl : 0) : W;
+            const int budget = fin ? m : W - O;
+            int d_min;
+            TbOut o{};
+            bool ok = true;
+            if (n == 0) {
+                if (m > K) {
+                    status = GA_WINDOW_FAILED;
+                    break;
+                }
+                d_min = m;
+                Planes pp = load_planes(P + p, m), tp{0, 0, 0};
+                ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, m, n, d_min,
+                               budget, lut, ops, nops, o);
+                tier_counts[2]++;
+            } else {
+                Planes pp = load_planes(P + p, m), tp = load_planes(T + t, n);
+                band.reset(n);
+                uint32_t okm = dc_band(pp, tp, m, n, band);
+                const int lim = K < 15 ? K : 15;
+                okm &= (2u << lim) - 1u;
+                if (okm) {
+                    d_min = __builtin_ctz(okm);
+                    ok = tb_band(band, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
+                    tier_counts[0]++;
+                } else if (K <= 15) {
+                    status = GA_WINDOW_FAILED;
+                    break;
+                } else {
+                    full.reset(K + kPassLevels + 1, W);
+                    d_min = dc_full(pp, tp, m, n, K, full);
+                    if (d_min < 0) {
+                        status = GA_WINDOW_FAILED;
+                        break;
+                    }
+                    ok = traceback([&](int e, int c, int x) { return full_bit(full, e, c, x); },
+                                   pp, tp, m, n, d_min, budget, lut, ops, nops, o);
+                    tier_counts[1]++;
+                }
+            }
+            if (!ok) {
+                status = GA_STUCK;
+                break;
+            }
+            const int64_t wr = window_writes(n, budget, K, d_min);
+            dists[widx] = (uint8_t)d_min;
+            r.rows_computed += d_min + 1;
+            r.cost += o.wcost;
+            r.entry_reads += o.reads;
+            r.entry_writes += wr;
+            r.words_allocated += wr * ((m + 63) / 64);
+            p += o.consumed;
+            t += o.tcons;
+            ++widx;
+        }
+        if (status != GA_OK) {
+            memset(&r, 0, sizeof r);
+            r.status = status;
+            r.fail_window = widx;
+            continue;
+        }
+        r.text_consumed = t;
+        r.ops_len = nops;
+    }
+    return 0;
+}
