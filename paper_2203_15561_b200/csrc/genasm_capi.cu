@@ -55,14 +55,17 @@ struct DevBuf {
 // so their kernels can overlap (the next chunk fills SMs as one drains).
 struct Scratch {
     unsigned long long* queue = nullptr;
-    uint32_t* overflow = nullptr;
+    uint32_t* overflow = nullptr;  // lane-group kernel
     size_t overflow_cap = 0;
+    uint32_t* thr = nullptr;       // lane-per-pair kernel
+    size_t thr_cap = 0;
     void release() {
         if (overflow) cudaFree(overflow);
+        if (thr) cudaFree(thr);
         if (queue) cudaFree(queue);
-        overflow = nullptr;
+        overflow = thr = nullptr;
         queue = nullptr;
-        overflow_cap = 0;
+        overflow_cap = thr_cap = 0;
     }
 };
 
@@ -272,18 +275,19 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     e = cudaMemsetAsync(sc->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
-    // GA_KERNEL=thread selects the lane-per-pair kernel (W <= 64); the
-    // lane-group kernel serves everything else
+    // W <= 64: the lane-per-pair kernel (which hands its outlier pairs to the
+    // lane-group kernel); GA_KERNEL=lockstep forces the lane-group kernel,
+    // which also serves W > 64
     const char* kern = getenv("GA_KERNEL");
-    const bool lockstep = P.W > 64 || !(kern && strcmp(kern, "thread") == 0);
+    const bool lockstep = P.W > 64 || (kern && strcmp(kern, "lockstep") == 0);
     if (lockstep) {
         const int group = env_int("GA_GROUP", 8);
         const int block = env_int("GA_BLOCK", 0);
         e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &sc->overflow,
                                            &sc->overflow_cap, &c->last_shape);
     } else {
-        e = genasm::launch_genasm_thread(P, c->num_sms, st, &sc->overflow, &sc->overflow_cap,
-                                         &c->last_shape);
+        e = genasm::launch_genasm_thread(P, c->num_sms, st, &sc->thr, &sc->thr_cap, &sc->overflow,
+                                         &sc->overflow_cap, &c->last_shape);
     }
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     return 0;
@@ -303,7 +307,7 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
     cudaStream_t st = stream_ptr ? (cudaStream_t)stream_ptr : c->stream;
     const int rc = launch_batch(c, in, cfg, out, st, &c->scratch);
-    if (rc == 0) c->launches = 1;
+    if (rc == 0) c->launches = c->last_shape.launches;
     return rc;
 }
 
@@ -457,7 +461,7 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
         dout.win_capacity = nwin;
         const int rc = launch_batch(c, &din, cfg, &dout, sk, &S.scratch);
         if (rc) return rc;
-        launches += 1;
+        launches += c->last_shape.launches;
         if (out->ops2) {
             if ((e = genasm::launch_pack_ops((const uint8_t*)S.ops.ptr, nops, (uint8_t*)S.ops2.ptr, sk)))
                 return fail(c, e, "pack kernel");

@@ -57,6 +57,8 @@ genasm_kernel(const KernelParams P) {
     int64_t cost = 0, rows = 0, reads = 0, writes = 0, words = 0;
 
     // called by all G lanes of the group
+    const unsigned long long n_eff = P.n_dev ? *P.n_dev : (unsigned long long)P.n_pairs;
+
     auto write_result = [&](int status, int fail_window) {
         if (status == 1 || status == 3) {  // windows the pair never completed read as 0
             const int64_t step = W - O;
@@ -88,7 +90,7 @@ genasm_kernel(const KernelParams P) {
             if (need && q == 0) idx = atomicAdd(P.queue, 1ull);
             idx = __shfl_sync(FULL, idx, 0, G);
             if (need) {
-                if (idx >= (unsigned long long)P.n_pairs) {
+                if (idx >= n_eff) {
                     phase = DONE;
                 } else {
                     pair = P.order ? (int64_t)P.order[idx] : (int64_t)idx;
@@ -101,6 +103,18 @@ genasm_kernel(const KernelParams P) {
                     p = t = nops = 0;
                     widx = 0;
                     cost = rows = reads = writes = words = 0;
+                    if (P.resume) {  // continue from the parked state
+                        const PairResult& r = results[pair];
+                        widx = r.fail_window;
+                        p = (int64_t)widx * (W - O);
+                        t = r.text_consumed;
+                        nops = r.ops_len;
+                        cost = r.cost;
+                        rows = r.rows_computed;
+                        reads = r.entry_reads;
+                        writes = r.entry_writes;
+                        words = r.words_allocated;
+                    }
                     if (Lp <= 0) write_result(2, -1);  // EmptyPattern (window.py:87-88)
                     else phase = NEED_WINDOW;
                 }
@@ -418,6 +432,7 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     shape->group = G;
     shape->blocks_per_sm = per_sm;
     shape->overflow_words_per_group = P.overflow_words_per_group;
+    shape->launches = 1;
     return cudaGetLastError();
 }
 

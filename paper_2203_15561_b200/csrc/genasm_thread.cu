@@ -13,8 +13,10 @@
 // diverges into the slow path.  When 32 hard windows are parked (or nothing
 // else is left) the warp runs them together: active pairs are parked on the
 // RESUME stack, each lane runs one hard window, the pairs go back on RESUME,
-// and free lanes refill from RESUME before taking fresh pairs from the global
-// queue (longest first).
+// and free lanes refill from RESUME before taking fresh pairs from the warp's
+// static share of the longest-first order (dealt round-robin across warps).  Parked pairs resume oldest first, and while pairs
+// wait the active ones rotate out every 8 windows: every pair of a warp
+// advances at the same pace, so the warp's pairs finish together.
 //
 // Tables.  Band tier: per warp, [column][word quad][lane] x 16 B -- each
 // column's 16 levels are 8 paired words (genasm_thread.cuh), two coalesced
@@ -25,11 +27,21 @@
 
 namespace genasm {
 
+#ifdef GA_THREAD_STATS
+// dev counters: band steps, active lanes summed over band steps, hard batches,
+// hard lanes summed over batches
+__device__ unsigned long long g_thread_stats[8];
+#define GA_STAT(k, v) (lane == 0 ? atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : 0ull)
+#else
+#define GA_STAT(k, v) 0ull
+#endif
+
 namespace {
 
 constexpr int kTBlock = 128;           // threads per block
 constexpr int kWarps = kTBlock / 32;
 constexpr int kStack = 128;            // per-warp HARD / RESUME stack entries
+constexpr int kHandoff = 24;           // full-tier windows before a pair is handed over
 constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
 
 struct BandTab {
@@ -61,7 +73,7 @@ struct FullTab {
 // per-lane pair state (between windows)
 struct Lane {
     int pair;  // -1: none
-    int Lp, Lt, widx;
+    int Lp, Lt, widx, hardc;  // hardc: windows that needed the full tier
     int64_t pat, txt, ops, dst;  // offsets
     int64_t t, nops, cost, rows, reads, writes, words;
 };
@@ -79,13 +91,14 @@ __device__ __forceinline__ void open_pair(const KernelParams& P, Lane& L, int pa
 __device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int pair) {
     open_pair(P, L, pair);
     L.widx = 0;
+    L.hardc = 0;
     L.t = L.nops = L.cost = L.rows = L.reads = L.writes = L.words = 0;
 }
 
 // park: the running state goes into the pair's own result record
 __device__ __forceinline__ void park(const KernelParams& P, const Lane& L) {
     PairResult* r = reinterpret_cast<PairResult*>(P.results) + L.pair;
-    r->status = -1;
+    r->status = -1 - L.hardc;
     r->fail_window = L.widx;
     r->cost = L.cost;
     r->text_consumed = L.t;
@@ -99,6 +112,7 @@ __device__ __forceinline__ void park(const KernelParams& P, const Lane& L) {
 __device__ __forceinline__ void unpark(const KernelParams& P, Lane& L, int pair) {
     open_pair(P, L, pair);
     const PairResult* r = reinterpret_cast<const PairResult*>(P.results) + pair;
+    L.hardc = -1 - r->status;
     L.widx = r->fail_window;
     L.cost = r->cost;
     L.t = r->text_consumed;
@@ -230,39 +244,43 @@ __global__ void __launch_bounds__(kTBlock)
 genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_base,
                      int64_t full_words_per_lane) {
     __shared__ int s_hard[kWarps][kStack], s_res[kWarps][kStack];
-    __shared__ int s_nh[kWarps], s_nr[kWarps];
+    __shared__ int s_nh[kWarps], s_rh[kWarps], s_rt[kWarps];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     BandTab bt{reinterpret_cast<uint4*>(band_base + gw * kBandWordsPerWarp), lane};
     FullTab ft{full_base + (gw * 32 + lane) * full_words_per_lane, P.W};
-    int* hard = s_hard[wib];
-    int* res = s_res[wib];
-    if (lane == 0) s_nh[wib] = s_nr[wib] = 0;
+    int* hard = s_hard[wib];  // stack of parked hard windows
+    int* res = s_res[wib];    // FIFO ring of parked pairs ready to resume
+    if (lane == 0) s_nh[wib] = s_rh[wib] = s_rt[wib] = 0;
     __syncwarp();
     const unsigned lt = lanemask_lt();
     bool exhausted = false;
+    int steps = 0;
+    int64_t taken = 0;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     Lane L;
     L.pair = -1;
     for (;;) {
-        // ---- free lanes take parked pairs first, then fresh ones (longest first) ----
+        // ---- free lanes take parked pairs first (oldest first), then fresh ones ----
         unsigned freem = __ballot_sync(FULL, L.pair < 0);
         if (freem) {
-            const int nr = s_nr[wib];
+            const int rh = s_rh[wib], nr = s_rt[wib] - rh;
             const int rank = __popc(freem & lt);
             const int take = min(__popc(freem), nr);
-            if (L.pair < 0 && rank < take) unpark(P, L, res[nr - 1 - rank]);
+            if (L.pair < 0 && rank < take) unpark(P, L, res[(rh + rank) & (kStack - 1)]);
             __syncwarp();
-            if (lane == 0) s_nr[wib] = nr - take;
+            if (lane == 0) s_rh[wib] = rh + take;
             freem = __ballot_sync(FULL, L.pair < 0);
             if (freem && !exhausted) {
+                // fresh pairs: this warp's static share of the longest-first
+                // order, dealt round-robin (every warp gets the same work)
                 const int cnt = __popc(freem);
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(P.queue, (unsigned long long)cnt);
-                base = __shfl_sync(FULL, base, 0);
-                if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
+                const int64_t k0 = taken;
+                taken += cnt;
+                if ((uint64_t)(gw + taken * nwarps) >= (uint64_t)P.n_pairs) exhausted = true;
                 if (L.pair < 0) {
-                    const unsigned long long idx = base + __popc(freem & lt);
-                    if (idx < (unsigned long long)P.n_pairs) {
+                    const uint64_t idx = (uint64_t)gw + (uint64_t)(k0 + __popc(freem & lt)) * nwarps;
+                    if (idx < (uint64_t)P.n_pairs) {
                         const int pair = P.order ? P.order[idx] : (int)idx;
                         fresh_pair(P, L, pair);
                         if (L.Lp <= 0) finish(P, L, 2);  // EmptyPattern (window.py:87-88)
@@ -272,32 +290,43 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_b
         }
         __syncwarp();
         const int nh = s_nh[wib];
+        const int nr = s_rt[wib] - s_rh[wib];
         const unsigned active = __ballot_sync(FULL, L.pair >= 0);
-        if (!active && nh == 0 && s_nr[wib] == 0 && exhausted) break;
+        if (!active && nh == 0 && nr == 0 && exhausted) break;
+        const int nact = __popc(active);
 
         // parked hard windows run as a batch once 32 wait, or once at least
-        // half of the warp's pairs in flight are parked (lanes would idle)
-        const int nact = __popc(active);
-        if (nh >= 32 || (nh > 0 && nh >= nact + s_nr[wib])) {
-            // ---- hard batch: park the active pairs, run up to 32 full-tier windows ----
-            int nr = s_nr[wib];
+        // half of the warp's pairs in flight are parked (lanes would idle);
+        // every 8 steps with pairs waiting, the active pairs also rotate out so
+        // that all pairs of the warp advance at the same pace (no long tail)
+        const bool batch = nh >= 32 || (nh > 0 && nh >= nact + nr);
+        const bool rotate = !batch && nr > 0 && nact > 0 && (++steps & 7) == 0;
+        if (batch || rotate) {
+            int rt = s_rt[wib];
             if (L.pair >= 0) {
                 park(P, L);
-                res[nr + __popc(active & lt)] = L.pair;
+                res[(rt + __popc(active & lt)) & (kStack - 1)] = L.pair;
                 L.pair = -1;
             }
-            nr += __popc(active);
-            const int take = nh < 32 ? nh : 32;
-            int hp = -1;
-            if (lane < take) {
-                hp = hard[nh - 1 - lane];
-                if (!hard_window(P, hp, bt.base, lane, ft.base)) hp = -1;
+            rt += nact;
+            int take = 0;
+            if (batch) {
+                // ---- hard batch: up to 32 full-tier windows, one per lane ----
+                take = nh < 32 ? nh : 32;
+                GA_STAT(2, 1);
+                GA_STAT(3, take);
+                int hp = -1;
+                if (lane < take) {
+                    hp = hard[nh - 1 - lane];
+                    if (!hard_window(P, hp, bt.base, lane, ft.base)) hp = -1;
+                }
+                const unsigned back = __ballot_sync(FULL, hp >= 0);
+                if (hp >= 0) res[(rt + __popc(back & lt)) & (kStack - 1)] = hp;
+                rt += __popc(back);
             }
-            const unsigned back = __ballot_sync(FULL, hp >= 0);
-            if (hp >= 0) res[nr + __popc(back & lt)] = hp;
             __syncwarp();
             if (lane == 0) {
-                s_nr[wib] = nr + __popc(back);
+                s_rt[wib] = rt;
                 s_nh[wib] = nh - take;
             }
             __syncwarp();
@@ -306,8 +335,18 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_b
         if (!active) continue;
 
         // ---- one band-tier window per active lane ----
+        GA_STAT(0, 1);
+        GA_STAT(1, nact);
         int r = WIN_NEXT;
         if (L.pair >= 0) r = run_window<false>(P, L, bt, ft);
+        // a pair whose windows keep needing the full tier (e.g. unrelated
+        // sequences) goes to the lane-group kernel instead of the hard stack
+        if (r == WIN_HARD && ++L.hardc > kHandoff) {
+            park(P, L);
+            P.handoff[atomicAdd(P.n_handoff, 1ull)] = L.pair;
+            L.pair = -1;
+            r = WIN_NEXT;
+        }
         const unsigned hm = __ballot_sync(FULL, r == WIN_HARD);
         if (hm) {
             if (r == WIN_HARD) {
@@ -322,9 +361,11 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_b
     }
 }
 
-cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_t stream,
-                                 uint32_t** scratch, size_t* cap, LaunchShape* shape) {
-    if (P.W > 64) return cudaErrorInvalidValue;
+cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStream_t stream,
+                                 uint32_t** scratch, size_t* cap, uint32_t** lock_scratch,
+                                 size_t* lock_cap, LaunchShape* shape) {
+    if (base.W > 64) return cudaErrorInvalidValue;
+    KernelParams P = base;
     int per_sm = 0;
     cudaError_t e =
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, genasm_thread_kernel, kTBlock, 0);
@@ -334,14 +375,21 @@ cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_
     const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 16;
     const int bcap = warps_cap / kWarps;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
-    int grid = num_sms * per_sm;
-    const int64_t max_useful = (P.n_pairs + kTBlock - 1) / kTBlock;
-    if (grid > max_useful) grid = (int)(max_useful > 0 ? max_useful : 1);
-    // full-tier rows: levels 0..k (+ a pass of slack) x W columns x 8 bytes per lane
+    // pairs are long sequential chains, so give every lane the same number of
+    // pairs: the fewest waves the resident lanes allow, then just enough warps
+    const int64_t resident = (int64_t)num_sms * per_sm * kTBlock;
+    const int64_t waves = (P.n_pairs + resident - 1) / resident;
+    const int64_t lanes = (P.n_pairs + waves - 1) / (waves > 0 ? waves : 1);
+    int grid = (int)((lanes + kTBlock - 1) / kTBlock);
+    if (grid < 1) grid = 1;
+    // scratch: band tables | full-tier rows (levels 0..k x W x 8 B per lane) |
+    // hand-over list (n_pairs ids) | its counter
     const int64_t full_words = (int64_t)(P.k + 1) * P.W * 2;
     const size_t warps = (size_t)grid * kWarps;
-    const size_t band_words = warps * kBandWordsPerWarp;
-    const size_t need = band_words + warps * 32 * (size_t)full_words + 64;
+    const size_t band_words = (warps * kBandWordsPerWarp + 63) & ~(size_t)63;
+    const size_t full_total = (warps * 32 * (size_t)full_words + 63) & ~(size_t)63;
+    const size_t list_words = ((size_t)P.n_pairs + 63) & ~(size_t)63;
+    const size_t need = band_words + full_total + list_words + 64;
     if (need > *cap || !*scratch) {
         if (*scratch) cudaFree(*scratch);
         *scratch = nullptr;
@@ -351,15 +399,38 @@ cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_
         *cap = need;
     }
     uint32_t* band = *scratch;
-    uint64_t* full = reinterpret_cast<uint64_t*>(*scratch + ((band_words + 63) & ~(size_t)63));
+    uint64_t* full = reinterpret_cast<uint64_t*>(*scratch + band_words);
+    P.handoff = reinterpret_cast<int32_t*>(*scratch + band_words + full_total);
+    P.n_handoff = reinterpret_cast<unsigned long long*>(*scratch + band_words + full_total +
+                                                        list_words);
+    if ((e = cudaMemsetAsync(P.n_handoff, 0, sizeof(unsigned long long), stream))) return e;
     genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, full, full_words / 2);
+    if ((e = cudaGetLastError())) return e;
+    // the handed-over pairs: lane-group kernel, resuming from the parked state
+    KernelParams R = P;
+    R.order = P.handoff;
+    R.n_dev = P.n_handoff;
+    R.resume = 1;
+    LaunchShape ls{};
+    e = launch_genasm_lockstep(R, 8, 0, num_sms, stream, lock_scratch, lock_cap, &ls);
     shape->grid = grid;
     shape->block = kTBlock;
     shape->smem_bytes = 0;
     shape->group = 1;
     shape->blocks_per_sm = per_sm;
     shape->overflow_words_per_group = full_words;
-    return cudaGetLastError();
+    shape->launches = 2;
+    return e;
 }
 
 }  // namespace genasm
+
+#ifdef GA_THREAD_STATS
+extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
+    }
+}
+#endif

@@ -231,3 +231,40 @@ def test_config3_full_vs_oracle(gpu, oracle_mod):
         assert got.cigar(q) == exp.ops[int(exp.ops_off[q]):int(exp.ops_off[q])
                                        + int(exp.results["ops_len"][q])].tobytes().decode(), q
     assert (got.results["status"] == 0).all()  # k = W: every window aligns
+
+
+@pytest.mark.parametrize("kernel", ["thread", "lockstep"])
+def test_both_kernels_vs_oracle(gpu, oracle_mod, monkeypatch, kernel):
+    """Each kernel on its own (GA_KERNEL): the lane-per-pair kernel with its
+    band / full tiers and hand-over, and the lane-group kernel."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    monkeypatch.setenv("GA_KERNEL", kernel)
+    batch, _ = sim.config_pairs(5)
+    for (w, o, k, prio) in [(64, 24, 64, "MSID"), (64, 24, 16, "DISM"), (32, 12, 32, "SMDI"),
+                            (48, 18, 30, "IDSM")]:
+        got = run_packed(batch, w, o, k, prio)
+        exp = oracle_mod.align_packed(batch, w, o, k, prio, threads=os.cpu_count())
+        _packed_equal(got, exp, (kernel, w, o, k, prio))
+    for (w, o, k, prio), pairs in corpus.fuzz_cases(99, 60, pairs_per_batch=16, max_len=500):
+        cfg = _cfg(gpu, w, o, k, prio)
+        got = [corpus.outcome_key(x) for x in gpu.align_batch(pairs, cfg)]
+        exp = [corpus.outcome_key(x) for x in oracle_mod.align_batch(pairs, cfg, threads=4)]
+        assert got == exp, (kernel, (w, o, k, prio))
+
+
+def test_handoff_of_unrelated_pairs(gpu, oracle_mod):
+    """Pairs whose windows all exceed the band tier (unrelated sequences) are
+    handed from the lane-per-pair kernel to the lane-group kernel mid-pair."""
+    from paper_2203_15561_b200._abi import PackedBatch
+    from paper_2203_15561_b200.engine import run_packed
+    rng = np.random.default_rng(12)
+    pairs = []
+    for q in range(300):
+        p = "".join(rng.choice(list("ACGT"), 3000))
+        t = "".join(rng.choice(list("ACGT"), 3000)) if q % 3 == 0 else p
+        pairs.append((p, t))
+    batch = PackedBatch.from_pairs(pairs)
+    got = run_packed(batch, 64, 24, 64, "MSID")
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    _packed_equal(got, exp, "handoff")

@@ -53,6 +53,12 @@ def main():
         st.synchronize()
         times.append(a.elapsed_time(b))
     r = res.cpu().numpy().view(_abi.RESULT_DTYPE)
+    if hasattr(L, "ga_debug_thread_stats"):
+        st = np.zeros(8, np.uint64)
+        L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
+        st = st.astype(np.float64) / reps
+        print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
+              f"hard batches {st[2]:.0f} lanes/batch {st[3] / max(st[2], 1):.2f}")
     print(f"config {cfg_id} n={n} ms/launch {[round(x, 2) for x in times]} "
           f"best {min(times):.2f} ({n / min(times) * 1e3 / 1e6:.3f} M aln/s) "
           f"status {np.bincount(r['status'], minlength=4).tolist()}", flush=True)
