@@ -70,6 +70,8 @@ struct KernelParams {
     // pairs the lane-per-pair kernel handed over)
     const unsigned long long* n_dev;
     int32_t resume;
+    int32_t full_only;     // every window starts with full-width rows (no band pass)
+    int32_t warps_per_sm;  // residency cap (0: GA_WARPS_PER_SM or the default)
     // lane-per-pair kernel only: hand-over list (pair ids) and its length
     int32_t* handoff;
     unsigned long long* n_handoff;

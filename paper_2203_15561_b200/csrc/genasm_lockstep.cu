@@ -5,6 +5,11 @@
 
 namespace genasm {
 
+template <int NW, int G>
+__host__ __device__ constexpr int smem_pad() {
+    return G * NW > 32 ? G * NW : 32;
+}
+
 template <int NW, int G, int LPL>
 __global__ void __launch_bounds__(kMaxBlock)
 genasm_kernel(const KernelParams P) {
@@ -23,8 +28,9 @@ genasm_kernel(const KernelParams P) {
     constexpr int LPP = G * LPL;                       // levels per pass
     constexpr int SMAX = WMAX + G - 1;                 // wavefront steps per pass
     constexpr int NPASS = BAND ? 1 : (LV + LPP - 1) / LPP;  // band-table passes
-    // 32-word pad: the wavefront's look-ahead loads reach G*NW words before a region
-    uint32_t* carry = smem + 32 + gib * (2 * WMAX * NW + WMAX / 2);
+    // pads: the wavefront's look-ahead loads reach G*NW words before a group's
+    // region and past its end (smem_pad<>)
+    uint32_t* carry = smem + smem_pad<NW, G>() + gib * (2 * WMAX * NW + WMAX / 2);
     uint32_t* pmcol = carry + WMAX * NW;
     uint8_t* cp = reinterpret_cast<uint8_t*>(pmcol + WMAX * NW);
     uint8_t* ct = cp + WMAX;
@@ -174,7 +180,7 @@ genasm_kernel(const KernelParams P) {
                     }
                 }
                 pass = 0;
-                full = false;
+                full = BAND && P.full_only;
                 if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
                     if (m <= K) {
                         d_min = m;
@@ -391,7 +397,8 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     KernelParams P = base;
     if (block < G || block > kMaxBlock || block % 32) block = G >= 16 ? 64 : 32;
     const int groups_per_block = block / G;
-    const int smem = (32 + groups_per_block * (2 * GE::WMAX * NW + GE::WMAX / 2)) * 4;
+    const int smem =
+        (2 * smem_pad<NW, G>() + groups_per_block * (2 * GE::WMAX * NW + GE::WMAX / 2)) * 4;
     auto kern = genasm_kernel<NW, G, LPL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -402,7 +409,8 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     // resident warps bound the band tables' L2 footprint (≈34 KB per warp at W=64,
     // G=4); measured best on config 3 with occupancy-limited residency (≈24 warps)
     const char* cap_env = getenv("GA_WARPS_PER_SM");
-    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 64;
+    const int warps_cap = P.warps_per_sm > 0 ? P.warps_per_sm
+                          : cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 64;
     const int bcap = warps_cap * 32 / block;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
     int grid = num_sms * per_sm;
@@ -445,6 +453,11 @@ static cudaError_t launch_nw(const KernelParams& P, int group, int block, int nu
         case 4: return launch_t<NW, 4, 4>(P, block, num_sms, stream, overflow, cap, shape);
         case 8: return launch_t<NW, 8, 2>(P, block, num_sms, stream, overflow, cap, shape);
         case 16: return launch_t<NW, 16, 1>(P, block, num_sms, stream, overflow, cap, shape);
+        // 32 lanes x 2 levels: 64 levels per pass, full-width rows only (the
+        // band table holds 16 levels) -- the latency-bound hand-over pairs
+        case 32:
+            if (!P.full_only) return cudaErrorInvalidValue;
+            return launch_t<NW, 32, 2>(P, block, num_sms, stream, overflow, cap, shape);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -411,8 +411,15 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     R.order = P.handoff;
     R.n_dev = P.n_handoff;
     R.resume = 1;
+    // latency-bound: 32-lane groups, 64 levels per pass, few warps per SM so a
+    // group's full-width rows stay in L1 for its traceback
+    R.full_only = P.W > 32;
+    const char* hg = getenv("GA_HANDOFF_GROUP");
+    const char* hw = getenv("GA_HANDOFF_WARPS");
+    R.warps_per_sm = hw && atoi(hw) > 0 ? atoi(hw) : 4;
     LaunchShape ls{};
-    e = launch_genasm_lockstep(R, 8, 0, num_sms, stream, lock_scratch, lock_cap, &ls);
+    e = launch_genasm_lockstep(R, hg && atoi(hg) > 0 ? atoi(hg) : (R.full_only ? 32 : 8), 0,
+                               num_sms, stream, lock_scratch, lock_cap, &ls);
     shape->grid = grid;
     shape->block = kTBlock;
     shape->smem_bytes = 0;
