@@ -31,9 +31,9 @@ namespace genasm {
 // dev counters: band steps, active lanes summed over band steps, hard batches,
 // hard lanes summed over batches
 __device__ unsigned long long g_thread_stats[8];
-#define GA_STAT(k, v) (lane == 0 ? atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : 0ull)
+#define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
-#define GA_STAT(k, v) 0ull
+#define GA_STAT(k, v) ((void)0)
 #endif
 
 namespace {
@@ -240,7 +240,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTBlock)
+#ifndef GA_THREAD_MINB
+#define GA_THREAD_MINB 4  // resident blocks per SM the register budget must allow
+#endif
+
+__global__ void __launch_bounds__(kTBlock, GA_THREAD_MINB)
 genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_base,
                      int64_t full_words_per_lane) {
     __shared__ int s_hard[kWarps][kStack], s_res[kWarps][kStack];

@@ -19,14 +19,15 @@
 // |delta| <= d_min - d <= 15 - d (and its predecessors at level d-1 have
 // |delta +- 1| <= 15 - (d-1)), and the success cell has delta = 0: all are
 // exact when each row is kept only on the 32 diagonals delta in [-16, 15],
-// everything outside treated as inactive.  Column j keeps absolute bits
-// [org_j, org_j + 31] with org_j = max(o_j, 0), o_j = m - n + j - 16.  Moving
-// one column right the band moves up one bit, so in band coordinates
+// everything outside treated as inactive.  Column j keeps bits
+// [o_j, o_j + 31], o_j = m - n + j - 16 (bits below 0 are virtual and stay
+// active, as the zeros sh() shifts in).  Moving one column right the band
+// moves up one bit, so in band coordinates
 //   M: sh(R[d][j-1])   -> R[d][j-1] unchanged      S: sh(R[d-1][j-1]) -> a
-//   I: sh(R[d-1][j])   -> (b << 1) | 1            D: R[d-1][j-1]     -> (a >> 1) | 2^31
-// (a = R[d-1][j-1], b = R[d-1][j]; the filled bits are out-of-band cells).
-// While o_j <= 0 the band is pinned at bit 0 and the plain recurrence
-// applies.  Four 32-bit operations per entry instead of 5 * ceil(m/32).
+//   I: sh(R[d-1][j])   -> (b << 1) | f            D: R[d-1][j-1]     -> (a >> 1) | 2^31
+// (a = R[d-1][j-1], b = R[d-1][j]; the filled bits are out-of-band cells,
+// f = 0 while the bit below the band is virtual).  Four 32-bit operations
+// per entry instead of 5 * ceil(m/32).
 //
 // Full tier (d_min > 15): full-width 64-bit rows, 4 levels per pass, rows
 // kept in a per-lane table for the traceback.
@@ -175,8 +176,7 @@ GA_HD uint32_t pm_word(uint32_t p0, uint32_t p1, uint32_t pn, const Planes& tp, 
 // diagonals |delta| <= 15 - e, i.e. band bits [e, 30-e]: 31-2e bits for level
 // e and 2e+1 bits for level 15-e, 32 together.  Rotated by 16, level 15-e's
 // bits [15-e, 15+e] land exactly on the bits level e leaves free, so word k
-// of a stored column holds levels k and 15-k (k = 0..7).  Columns whose band
-// is pinned at bit 0 are first shifted to virtual band coordinates.
+// of a stored column holds levels k and 15-k (k = 0..7).
 GA_HD uint32_t rot16(uint32_t x) {
 #ifdef __CUDA_ARCH__
     return __byte_perm(x, 0, 0x1032);
@@ -188,17 +188,6 @@ GA_HD uint32_t pair_word(uint32_t lo, uint32_t hi, int k) {
     const uint32_t mk = ((1u << (31 - 2 * k)) - 1u) << k;  // bits [k, 30-k]
     return (lo & mk) | (rot16(hi) & ~mk);
 }
-template <class Tab>
-GA_HD void put_packed(Tab& tab, int j, const uint32_t* col, int shl) {
-    uint32_t w[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t lo = shl ? (shl < 32 ? col[k] << shl : 0u) : col[k];
-        const uint32_t hi = shl ? (shl < 32 ? col[15 - k] << shl : 0u) : col[15 - k];
-        w[k] = pair_word(lo, hi, k);
-    }
-    tab.put(j, w);
-}
 // stored bit at band position b of level e (0 <= e <= 15) from a column's words
 GA_HD uint32_t packed_bit(uint32_t w_lo_or_hi, int e, int b) {
     const int pos = e <= 7 ? b : b + 16;
@@ -206,39 +195,56 @@ GA_HD uint32_t packed_bit(uint32_t w_lo_or_hi, int e, int b) {
 }
 GA_HD int packed_word(int e) { return e <= 7 ? e : 15 - e; }
 
-// Band tier DC over columns 1..n of a window (m, n >= 1).  col[] ends as
-// R[d][n] (band at org_n); tab.put(j, w) receives each column's 8 paired
-// words.  Returns the mask of levels d <= 15 with R[d][n] bit m-1 active.
+// (b << 1) | f in one instruction (LEA)
+GA_HD uint32_t shl1_or(uint32_t b, uint32_t f) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(b), "r"(f));
+    return r;
+#else
+    return (b << 1) | f;
+#endif
+}
+
+// Band tier DC over columns 1..n of a window (m, n >= 1), every column in its
+// virtual band [o_j, o_j + 31]: band bits below absolute bit 0 are virtual
+// and stay 0 (active), exactly the zeros sh() shifts in, so one recurrence
+// serves every column -- only the I-edge fill differs (the bit below the band
+// is virtual, 0, while o_j <= 0 and an out-of-band 1 after) and the mismatch
+// word is masked to real bits.  col[] ends as R[d][n]; tab.put(j, w) receives
+// each column's 8 paired words.  Returns the mask of levels d <= 15 with
+// R[d][n] bit m-1 active.
 template <class Tab>
 GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& tab) {
     uint32_t col[kFastLevels];
     const int o0 = m - n - 16;
-    const int org0 = o0 > 0 ? o0 : 0;
 #pragma unroll
-    for (int d = 0; d < kFastLevels; ++d) col[d] = init_band(m, d, org0);
-    const uint32_t p0lo = (uint32_t)pp.b0, p1lo = (uint32_t)pp.b1, pnlo = (uint32_t)pp.bn;
-    // columns whose band is pinned at bit 0 (o_j <= 0): the plain recurrence
+    for (int d = 0; d < kFastLevels; ++d) col[d] = init_band(m, d, o0);
+    uint32_t w[8];
+    // columns with o_j <= 0: the band reaches below bit 0
     int jA = -o0;
     jA = jA < 0 ? 0 : (jA > n ? n : jA);
     for (int j = 1; j <= jA; ++j) {
-        const uint32_t pm = pm_word(p0lo, p1lo, pnlo, tp, j - 1);
+        const int sh = -(o0 + j);  // virtual bits at the bottom of the band
+        const uint32_t valid = sh < 32 ? ~0u << sh : 0u;
+        const uint32_t pm = pm_word((uint32_t)(pp.b0 << sh), (uint32_t)(pp.b1 << sh),
+                                    (uint32_t)(pp.bn << sh), tp, j - 1) & valid;
         uint32_t a = col[0];
-        uint32_t xa = a << 1;
-        uint32_t b = xa | pm;
+        uint32_t b = a | pm;
         col[0] = b;
 #pragma unroll
         for (int d = 1; d < kFastLevels; ++d) {
             const uint32_t c = col[d];
-            const uint32_t x = c << 1;
-            const uint32_t nc = and3(orand(x, pm, xa), b << 1, a);
+            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), shl1_or(b, 0u));
             a = c;
-            xa = x;
             col[d] = nc;
             b = nc;
         }
-        put_packed(tab, j, col, -(o0 + j));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
+        tab.put(j, w);
     }
-    // banded columns: origin o_j = o0 + j >= 1; four operations per entry
+    // columns with o_j >= 1; four operations per entry
 #pragma unroll 2
     for (int j = jA + 1; j <= n; ++j) {
         const int oj = o0 + j;
@@ -250,18 +256,19 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& ta
 #pragma unroll
         for (int d = 1; d < kFastLevels; ++d) {
             const uint32_t c = col[d];
-            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), 2u * b + 1u);
+            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), shl1_or(b, 1u));
             a = c;
             col[d] = nc;
             b = nc;
         }
-        put_packed(tab, j, col, 0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
+        tab.put(j, w);
     }
-    // success bit m-1 sits at band bit m-1-org_n = min(m-1, 15)
-    const int sb = m - 1 < 15 ? m - 1 : 15;
+    // success bit m-1 sits at band bit m-1-o_n = 15
     uint32_t ok = 0;
 #pragma unroll
-    for (int d = 0; d < kFastLevels; ++d) ok |= ((~col[d] >> sb) & 1u) << d;
+    for (int d = 0; d < kFastLevels; ++d) ok |= ((~col[d] >> 15) & 1u) << d;
     return ok;
 }
 
@@ -387,6 +394,31 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
 // Traceback of a band-tier window: the walk of traceback() with the level
 // bits read from the paired band words (positions relative to each column's
 // virtual band origin o_j) and the '=' test from the symbol planes.
+GA_HD unsigned ctz32(unsigned x) {  // count trailing zeros, x != 0
+#ifdef __CUDA_ARCH__
+    return __ffs(x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+
+// symbol equality along a diagonal: bit x = (cp[x + s] == ct[x]), both in ACGT
+GA_HD uint64_t diag_eq(const Planes& pp, const Planes& tp, int s) {
+    uint64_t a0, a1, an;
+    if (s >= 0) {
+        a0 = s < 64 ? pp.b0 >> s : 0ull;
+        a1 = s < 64 ? pp.b1 >> s : 0ull;
+        an = s < 64 ? pp.bn >> s : ~0ull;
+    } else {
+        a0 = -s < 64 ? pp.b0 << -s : 0ull;
+        a1 = -s < 64 ? pp.b1 << -s : 0ull;
+        an = -s < 64 ? pp.bn << -s : ~0ull;
+    }
+    return ~((a0 ^ tp.b0) | (a1 ^ tp.b1) | an | tp.bn);
+}
+
+constexpr int kRun = 8;  // '=' steps speculated per round trip
+
 template <class Tab>
 GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
                    int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
@@ -395,6 +427,12 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
     const int o0 = m - n - 16;
     o.consumed = o.tcons = o.wcost = 0;
     o.reads = 0;
+    // with '=' first in priority a step is '=' iff its match edge is active:
+    // runs of them along a diagonal are found kRun at a time, their table
+    // words loaded together
+    const bool m_first = ((prio_lut >> 60) & 0xFu) == OPC_M;  // all four edges active -> M
+    int s_eq = 1 << 30;
+    uint64_t eqv = 0;
     for (;;) {
         if (i < 0 || o.consumed >= budget) return true;
         if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
@@ -406,6 +444,42 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             o.consumed += take;
             return true;
         }
+        if (m_first && j >= 2 && i >= 1) {
+            int K = j - 1;
+            K = K < i ? K : i;
+            K = K < budget - o.consumed ? K : budget - o.consumed;
+            K = K < kRun ? K : kRun;
+            const int sd = i - (j - 1);  // diagonal: pattern index - text index
+            if (sd != s_eq) {
+                s_eq = sd;
+                eqv = diag_eq(pp, tp, sd);
+            }
+            const int u = i - (o0 + j);
+            const int kd = packed_word(d);
+            uint32_t w[kRun];
+#pragma unroll
+            for (int k = 0; k < kRun; ++k) w[k] = k < K ? tab.get(kd, j - 1 - k) : 0u;
+            // step k sits at (i-k, j-k): '=' iff symbols match and R[d][j-1-k] bit i-1-k
+            // (band position u) is active
+            unsigned okm = 0;
+#pragma unroll
+            for (int k = 0; k < kRun; ++k) {
+                const uint32_t eq = (uint32_t)(eqv >> ((j - 1 - k) & 63)) & 1u;
+                okm |= (eq & ~packed_bit(w[k], d, u)) << k;
+            }
+            okm &= (1u << K) - 1u;
+            const int run = (int)ctz32(~okm);
+            for (int k = 0; k < run; ++k) ops[nops + k] = '=';
+            nops += run;
+            j -= run;
+            i -= run;
+            o.consumed += run;
+            o.tcons += run;
+            o.reads += (int64_t)run * (d > 0 ? 3 : 1);
+            if (run == K) continue;  // limits reached: re-check at the new state
+        }
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) continue;
         const int u = i - (o0 + j);  // band position of (i, j); (i-1, j-1) shares it
         const int dm1 = d > 0 ? d - 1 : 0;
         const uint32_t wj = tab.get(packed_word(dm1), j);
