@@ -246,6 +246,7 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
         return fail(c, e, "cudaMalloc");
     genasm::KernelParams P{};
     P.codes = in->codes;
+    P.codes_len = in->codes_len;
     P.pat_off = in->pat_off;
     P.pat_len = in->pat_len;
     P.txt_off = in->txt_off;

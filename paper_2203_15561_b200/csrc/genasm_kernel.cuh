@@ -47,6 +47,11 @@ namespace genasm {
 
 struct KernelParams {
     const uint8_t* codes;
+    int64_t codes_len;         // symbols in codes
+    // lane-per-pair kernel: the codes as three bit-planes (bit 0, bit 1, code 4),
+    // plane_words 64-bit words each, built per launch by a streaming kernel
+    const uint64_t* planes;
+    int64_t plane_words;
     const int64_t* pat_off;
     const int32_t* pat_len;
     const int64_t* txt_off;

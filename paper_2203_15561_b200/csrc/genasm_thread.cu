@@ -60,15 +60,22 @@ struct BandTab {
 };
 
 struct FullTab {
-    uint64_t* base;  // this lane's rows, [level][column 1..W]
-    int W;
-    __device__ __forceinline__ void put(int d, int j, uint64_t v) {
-        base[(size_t)d * W + (j - 1)] = v;
+    uint64_t* base;  // this lane's rows, [column 1..W][level 0..LV)
+    int LV;
+    __device__ __forceinline__ void put4(int d0, int j, const uint32_t* lo, const uint32_t* hi) {
+        uint4* p = reinterpret_cast<uint4*>(base + (size_t)(j - 1) * LV + d0);
+        p[0] = make_uint4(lo[0], hi[0], lo[1], hi[1]);
+        p[1] = make_uint4(lo[2], hi[2], lo[3], hi[3]);
     }
     __device__ __forceinline__ uint64_t get(int d, int j) const {
-        return base[(size_t)d * W + (j - 1)];
+        return base[(size_t)(j - 1) * LV + d];
     }
 };
+
+// full-tier rows stored per column: levels 0..k rounded up to whole passes
+__host__ __device__ __forceinline__ int full_levels(int k) {
+    return (k + thr::kPassLevels) / thr::kPassLevels * thr::kPassLevels;
+}
 
 // per-lane pair state (between windows)
 struct Lane {
@@ -162,7 +169,7 @@ __device__ __forceinline__ int run_window(const KernelParams& P, Lane& L, BandTa
     const int64_t tl = L.Lt - L.t;
     const int n = tl < W ? (int)(tl > 0 ? tl : 0) : W;
     const int budget = fin ? m : W - P.O;
-    const Planes pp = load_planes(P.codes + L.pat + p, m);
+    const Planes pp = load_planes_bits(P.planes, P.plane_words, L.pat + p, m);
     Planes tp{0ull, 0ull, 0ull};
     int d_min;
     uint8_t* ops = P.ops + L.ops;
@@ -177,7 +184,7 @@ __device__ __forceinline__ int run_window(const KernelParams& P, Lane& L, BandTa
         ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, m, n, d_min, budget,
                        P.prio_lut, ops, L.nops, o);
     } else {
-        tp = load_planes(P.codes + L.txt + L.t, n);
+        tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, n);
         if (!FULL) {
             uint32_t okm = dc_band(pp, tp, m, n, bt);
             const int lim = K < 15 ? K : 15;
@@ -225,7 +232,7 @@ __device__ __forceinline__ bool hard_window(const KernelParams& P, int pair, uin
     Lane L;
     unpark(P, L, pair);
     BandTab bt{band, lane};
-    FullTab ft{full, P.W};
+    FullTab ft{full, full_levels(P.k)};
     run_window<true>(P, L, bt, ft);
     if (L.pair < 0) return false;
     park(P, L);
@@ -240,6 +247,42 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 }  // namespace
 
+// codes -> three bit-planes: thread t packs symbols [64t, 64t+64) of each
+// plane into one 64-bit word (bit 0 of the code, bit 1, code 4)
+__global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__ codes, int64_t n,
+                                                     uint64_t* __restrict__ pl, int64_t words) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t f0 = 0, f1 = 0, fn = 0;
+        const int64_t s0 = t * 64;
+        if (s0 + 64 <= n && ((reinterpret_cast<uintptr_t>(codes) & 15) == 0)) {
+            const uint4* q = reinterpret_cast<const uint4*>(codes + s0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const uint4 x = __ldg(q + v);
+                const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int pos = 16 * v + 4 * u;
+                    f0 |= (uint64_t)thr::nib(w4[u], 0) << pos;
+                    f1 |= (uint64_t)thr::nib(w4[u], 1) << pos;
+                    fn |= (uint64_t)thr::nib(w4[u], 2) << pos;
+                }
+            }
+        } else {
+            for (int k = 0; k < 64 && s0 + k < n; ++k) {
+                const uint8_t c = codes[s0 + k];
+                f0 |= (uint64_t)(c & 1) << k;
+                f1 |= (uint64_t)((c >> 1) & 1) << k;
+                fn |= (uint64_t)((c >> 2) & 1) << k;
+            }
+        }
+        pl[t] = f0;
+        pl[words + t] = f1;
+        pl[2 * words + t] = fn;
+    }
+}
+
 #ifndef GA_THREAD_MINB
 #define GA_THREAD_MINB 4  // resident blocks per SM the register budget must allow
 #endif
@@ -252,7 +295,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_b
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     BandTab bt{reinterpret_cast<uint4*>(band_base + gw * kBandWordsPerWarp), lane};
-    FullTab ft{full_base + (gw * 32 + lane) * full_words_per_lane, P.W};
+    FullTab ft{full_base + (gw * 32 + lane) * full_words_per_lane, full_levels(P.k)};
     int* hard = s_hard[wib];  // stack of parked hard windows
     int* res = s_res[wib];    // FIFO ring of parked pairs ready to resume
     if (lane == 0) s_nh[wib] = s_rh[wib] = s_rt[wib] = 0;
@@ -386,14 +429,17 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     const int64_t lanes = (P.n_pairs + waves - 1) / (waves > 0 ? waves : 1);
     int grid = (int)((lanes + kTBlock - 1) / kTBlock);
     if (grid < 1) grid = 1;
-    // scratch: band tables | full-tier rows (levels 0..k x W x 8 B per lane) |
+    // scratch: band tables | full-tier rows (W x levels x 8 B per lane) |
     // hand-over list (n_pairs ids) | its counter
-    const int64_t full_words = (int64_t)(P.k + 1) * P.W * 2;
+    const int64_t full_words = (int64_t)full_levels(P.k) * P.W * 2;
     const size_t warps = (size_t)grid * kWarps;
     const size_t band_words = (warps * kBandWordsPerWarp + 63) & ~(size_t)63;
     const size_t full_total = (warps * 32 * (size_t)full_words + 63) & ~(size_t)63;
     const size_t list_words = ((size_t)P.n_pairs + 63) & ~(size_t)63;
-    const size_t need = band_words + full_total + list_words + 64;
+    // bit-planes: one word per 64 symbols per plane, plus one word of slack
+    const int64_t pw = (P.codes_len + 63) / 64 + 1;
+    const size_t plane_total = ((size_t)pw * 3 * 2 + 63) & ~(size_t)63;
+    const size_t need = band_words + full_total + list_words + 64 + plane_total;
     if (need > *cap || !*scratch) {
         if (*scratch) cudaFree(*scratch);
         *scratch = nullptr;
@@ -408,6 +454,15 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     P.n_handoff = reinterpret_cast<unsigned long long*>(*scratch + band_words + full_total +
                                                         list_words);
     if ((e = cudaMemsetAsync(P.n_handoff, 0, sizeof(unsigned long long), stream))) return e;
+    uint64_t* planes = reinterpret_cast<uint64_t*>(*scratch + band_words + full_total + list_words + 64);
+    P.planes = planes;
+    P.plane_words = pw;
+    {
+        const int64_t blocks = (pw + 255) / 256;
+        planes_kernel<<<(int)(blocks < 148 * 8 ? (blocks > 0 ? blocks : 1) : 148 * 8), 256, 0, stream>>>(
+            P.codes, P.codes_len, planes, pw);
+        if ((e = cudaGetLastError())) return e;
+    }
     genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, full, full_words / 2);
     if ((e = cudaGetLastError())) return e;
     // the handed-over pairs: lane-group kernel, resuming from the parked state
@@ -430,7 +485,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     shape->group = 1;
     shape->blocks_per_sm = per_sm;
     shape->overflow_words_per_group = full_words;
-    shape->launches = 2;
+    shape->launches = 3;
     return e;
 }
 

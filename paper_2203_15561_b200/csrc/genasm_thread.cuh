@@ -111,6 +111,30 @@ GA_HD Planes load_planes(const uint8_t* src, int len) {
     return p;
 }
 
+// planes of symbols [start, start+len), 1 <= len <= 64, from the bit-plane
+// form of the codes (bit x of word x/64 of each plane), reversed
+GA_HD Planes load_planes_bits(const uint64_t* pl, int64_t plane_words, int64_t start, int len) {
+    const int64_t wi = start >> 6;
+    const int r = (int)(start & 63);
+    uint64_t f[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const uint64_t* q = pl + k * plane_words + wi;
+#ifdef __CUDA_ARCH__
+        const uint64_t w0 = __ldg(q), w1 = __ldg(q + 1);
+#else
+        const uint64_t w0 = q[0], w1 = q[1];
+#endif
+        f[k] = r ? (w0 >> r) | (w1 << (64 - r)) : w0;
+    }
+    const int s = 64 - len;
+    Planes p;
+    p.b0 = brev64(f[0]) >> s;
+    p.b1 = brev64(f[1]) >> s;
+    p.bn = brev64(f[2]) >> s;
+    return p;
+}
+
 GA_HD uint32_t bit64(uint64_t x, int k) { return (uint32_t)(x >> k) & 1u; }
 
 // all-ones iff bit k of x
@@ -272,46 +296,77 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& ta
     return ok;
 }
 
-// Full tier DC: passes of 4 levels over full 64-bit rows, rows stored in
-// `ht` (level-major) for the traceback.  Returns d_min <= K or -1.
+// (hi:lo) << 1, the high word of a 64-bit row shift
+GA_HD uint32_t shl1_hi(uint32_t lo, uint32_t hi) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_l(lo, hi, 1);
+#else
+    return (hi << 1) | (lo >> 31);
+#endif
+}
+
+// Full tier DC: full-width rows (two 32-bit words, W <= 64), passes of
+// kPassLevels levels; every column's rows go to `ht` (column-major:
+// ht.put4(d0, j, lo, hi) stores levels d0..d0+3 of column j) for the
+// traceback and for the next pass.  Returns d_min <= K or -1.
 template <class HTab>
 GA_HD int dc_full(const Planes& pp, const Planes& tp, int m, int n, int K, HTab& ht) {
-    uint64_t pmask[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-        pmask[s] = (pp.b0 ^ (0ull - (uint64_t)(s & 1))) | (pp.b1 ^ (0ull - (uint64_t)(s >> 1))) |
-                   pp.bn;
-    const uint64_t tb = 1ull << (m - 1);
+    const uint32_t p0l = (uint32_t)pp.b0, p0h = (uint32_t)(pp.b0 >> 32);
+    const uint32_t p1l = (uint32_t)pp.b1, p1h = (uint32_t)(pp.b1 >> 32);
+    const uint32_t pnl = (uint32_t)pp.bn, pnh = (uint32_t)(pp.bn >> 32);
+    const bool thi = m - 1 >= 32;
+    const uint32_t tbit = 1u << ((m - 1) & 31);
     for (int d0 = 0; d0 <= K; d0 += kPassLevels) {
-        uint64_t col[kPassLevels];
+        uint32_t cl[kPassLevels], ch[kPassLevels];
 #pragma unroll
-        for (int k = 0; k < kPassLevels; ++k) col[k] = init_row64(m, d0 + k);
-        uint64_t aprev = d0 > 0 ? init_row64(m, d0 - 1) : 0ull;
-        // rows of level d0-1, loaded two columns ahead
+        for (int k = 0; k < kPassLevels; ++k) {
+            const uint64_t r = init_row64(m, d0 + k);
+            cl[k] = (uint32_t)r;
+            ch[k] = (uint32_t)(r >> 32);
+        }
+        const uint64_t a0 = d0 > 0 ? init_row64(m, d0 - 1) : 0ull;
+        uint32_t apl = (uint32_t)a0, aph = (uint32_t)(a0 >> 32);  // R[d0-1][j-1]
+        // rows of level d0-1 (previous pass), loaded two columns ahead
         uint64_t bl1 = d0 > 0 ? ht.get(d0 - 1, 1) : 0ull;
         uint64_t bl2 = (d0 > 0 && n >= 2) ? ht.get(d0 - 1, 2) : 0ull;
         for (int j = 1; j <= n; ++j) {
-            const uint64_t bl = bl1;
+            const uint64_t bcur = bl1;
             bl1 = bl2;
             bl2 = (d0 > 0 && j + 2 <= n) ? ht.get(d0 - 1, j + 2) : 0ull;
-            const int s = (int)(bit64(tp.b0, j - 1) | bit64(tp.b1, j - 1) << 1);
-            const uint64_t pm = bit64(tp.bn, j - 1) ? ~0ull : pmask[s];
-            uint64_t a = aprev, b = bl;
+            const uint32_t s0 = bcast(tp.b0, j - 1), s1 = bcast(tp.b1, j - 1),
+                           sn = bcast(tp.bn, j - 1);
+            const uint32_t pml = (p0l ^ s0) | (p1l ^ s1) | pnl | sn;
+            const uint32_t pmh = (p0h ^ s0) | (p1h ^ s1) | pnh | sn;
+            uint32_t al = apl, ah = aph;                      // R[d-1][j-1]
+            uint32_t xal = al << 1, xah = shl1_hi(al, ah);    // sh(R[d-1][j-1])
+            uint32_t bl = (uint32_t)bcur, bh = (uint32_t)(bcur >> 32);  // R[d-1][j]
 #pragma unroll
             for (int k = 0; k < kPassLevels; ++k) {
-                const uint64_t c = col[k];
-                const uint64_t nc = (d0 + k == 0) ? ((c << 1) | pm)
-                                                  : (((c << 1) | pm) & ((a & b) << 1) & a);
-                a = c;
-                b = nc;
-                col[k] = nc;
-                if (d0 + k <= K) ht.put(d0 + k, j, nc);
+                const uint32_t xl = cl[k] << 1, xh = shl1_hi(cl[k], ch[k]);
+                uint32_t nl, nh;
+                if (k == 0 && d0 == 0) {  // level 0: the match edge only
+                    nl = xl | pml;
+                    nh = xh | pmh;
+                } else {
+                    nl = and3(orand(xl, pml, xal), bl << 1, al);
+                    nh = and3(orand(xh, pmh, xah), shl1_hi(bl, bh), ah);
+                }
+                al = cl[k];
+                ah = ch[k];
+                xal = xl;
+                xah = xh;
+                bl = nl;
+                bh = nh;
+                cl[k] = nl;
+                ch[k] = nh;
             }
-            aprev = bl;
+            ht.put4(d0, j, cl, ch);
+            apl = (uint32_t)bcur;
+            aph = (uint32_t)(bcur >> 32);
         }
 #pragma unroll
         for (int k = 0; k < kPassLevels; ++k)
-            if (d0 + k <= K && !(col[k] & tb)) return d0 + k;
+            if (d0 + k <= K && !((thi ? ch[k] : cl[k]) & tbit)) return d0 + k;
     }
     return -1;
 }
@@ -320,6 +375,31 @@ template <class HTab>
 GA_HD uint32_t full_bit(HTab& ht, int e, int c, int x) {
     return (uint32_t)(ht.get(e, c) >> x) & 1u;
 }
+
+GA_HD unsigned ctz32(unsigned x) {  // count trailing zeros, x != 0
+#ifdef __CUDA_ARCH__
+    return __ffs(x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+
+// symbol equality along a diagonal: bit x = (cp[x + s] == ct[x]), both in ACGT
+GA_HD uint64_t diag_eq(const Planes& pp, const Planes& tp, int s) {
+    uint64_t a0, a1, an;
+    if (s >= 0) {
+        a0 = s < 64 ? pp.b0 >> s : 0ull;
+        a1 = s < 64 ? pp.b1 >> s : 0ull;
+        an = s < 64 ? pp.bn >> s : ~0ull;
+    } else {
+        a0 = -s < 64 ? pp.b0 << -s : 0ull;
+        a1 = -s < 64 ? pp.b1 << -s : 0ull;
+        an = -s < 64 ? pp.bn << -s : ~0ull;
+    }
+    return ~((a0 ^ tp.b0) | (a1 ^ tp.b1) | an | tp.bn);
+}
+
+constexpr int kRun = 8;  // '=' steps speculated per round trip
 
 // Traceback of one window (backtrace.py:88-160), from (j=n, d=d_min, i=m-1)
 // until the budget is consumed.  BIT(e, c, x) returns table bit x of level e,
@@ -336,6 +416,9 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
     int d = d_min, j = n, i = m - 1;
     o.consumed = o.tcons = o.wcost = 0;
     o.reads = 0;
+    const bool m_first = ((prio_lut >> 60) & 0xFu) == OPC_M;  // all four edges active -> M
+    int s_eq = 1 << 30;
+    uint64_t eqv = 0;
     for (;;) {
         if (i < 0 || o.consumed >= budget) return true;
         if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
@@ -346,6 +429,35 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
             o.wcost += take;
             o.consumed += take;
             return true;
+        }
+        if (m_first && j >= 2 && i >= 1) {  // a run of '=' steps, kRun reads in flight
+            int K = j - 1;
+            K = K < i ? K : i;
+            K = K < budget - o.consumed ? K : budget - o.consumed;
+            K = K < kRun ? K : kRun;
+            const int sd = i - (j - 1);
+            if (sd != s_eq) {
+                s_eq = sd;
+                eqv = diag_eq(pp, tp, sd);
+            }
+            uint32_t mbk[kRun];
+#pragma unroll
+            for (int k = 0; k < kRun; ++k) mbk[k] = k < K ? BIT(d, j - 1 - k, i - 1 - k) : 1u;
+            unsigned okm = 0;
+#pragma unroll
+            for (int k = 0; k < kRun; ++k)
+                okm |= (((uint32_t)(eqv >> ((j - 1 - k) & 63)) & 1u) & ~mbk[k]) << k;
+            okm &= (1u << K) - 1u;
+            const int run = (int)ctz32(~okm);
+            for (int k = 0; k < run; ++k) ops[nops + k] = '=';
+            nops += run;
+            j -= run;
+            i -= run;
+            o.consumed += run;
+            o.tcons += run;
+            o.reads += (int64_t)run * (d > 0 ? 3 : 1);
+            if (run == K) continue;
+            if (i < 0 || o.consumed >= budget) return true;
         }
         const bool symeq = !bit64(tp.bn, j - 1) && !bit64(pp.bn, i) &&
                            bit64(tp.b0, j - 1) == bit64(pp.b0, i) &&
@@ -394,30 +506,6 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
 // Traceback of a band-tier window: the walk of traceback() with the level
 // bits read from the paired band words (positions relative to each column's
 // virtual band origin o_j) and the '=' test from the symbol planes.
-GA_HD unsigned ctz32(unsigned x) {  // count trailing zeros, x != 0
-#ifdef __CUDA_ARCH__
-    return __ffs(x) - 1;
-#else
-    return __builtin_ctz(x);
-#endif
-}
-
-// symbol equality along a diagonal: bit x = (cp[x + s] == ct[x]), both in ACGT
-GA_HD uint64_t diag_eq(const Planes& pp, const Planes& tp, int s) {
-    uint64_t a0, a1, an;
-    if (s >= 0) {
-        a0 = s < 64 ? pp.b0 >> s : 0ull;
-        a1 = s < 64 ? pp.b1 >> s : 0ull;
-        an = s < 64 ? pp.bn >> s : ~0ull;
-    } else {
-        a0 = -s < 64 ? pp.b0 << -s : 0ull;
-        a1 = -s < 64 ? pp.b1 << -s : 0ull;
-        an = -s < 64 ? pp.bn << -s : ~0ull;
-    }
-    return ~((a0 ^ tp.b0) | (a1 ^ tp.b1) | an | tp.bn);
-}
-
-constexpr int kRun = 8;  // '=' steps speculated per round trip
 
 template <class Tab>
 GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
@@ -456,9 +544,17 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             }
             const int u = i - (o0 + j);
             const int kd = packed_word(d);
-            uint32_t w[kRun];
+            const int dm1 = d > 0 ? d - 1 : 0;
+            const int ke = packed_word(dm1);
+            // level d and d-1 words of columns j-1-k; level d-1 of column j too: the
+            // step that ends the run reads from them as well
+            uint32_t w[kRun], v[kRun];
 #pragma unroll
-            for (int k = 0; k < kRun; ++k) w[k] = k < K ? tab.get(kd, j - 1 - k) : 0u;
+            for (int k = 0; k < kRun; ++k) {
+                w[k] = k < K ? tab.get(kd, j - 1 - k) : 0u;
+                v[k] = k < K ? tab.get(ke, j - 1 - k) : 0u;
+            }
+            const uint32_t vj = tab.get(ke, j);
             // step k sits at (i-k, j-k): '=' iff symbols match and R[d][j-1-k] bit i-1-k
             // (band position u) is active
             unsigned okm = 0;
@@ -477,6 +573,31 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             o.tcons += run;
             o.reads += (int64_t)run * (d > 0 ? 3 : 1);
             if (run == K) continue;  // limits reached: re-check at the new state
+            // the step at (i, j) = run end: its '=' edge is inactive; the others
+            // come from the words already loaded (j >= 2, i >= 1 here)
+            uint32_t wr = v[0], wp = vj;
+#pragma unroll
+            for (int k = 1; k < kRun; ++k) {
+                wr = run == k ? v[k] : wr;
+                wp = run == k ? v[k - 1] : wp;
+            }
+            const bool dpos = d > 0;
+            const bool sok = dpos && !packed_bit(wr, dm1, u);
+            const bool iok = dpos && !packed_bit(wp, dm1, u - 1);
+            const bool dok = dpos && !packed_bit(wr, dm1, u + 1);
+            const unsigned om = (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+            const int op = (int)((prio_lut >> (4 * om)) & 0xFu);
+            o.reads += dpos ? 3 : 1;
+            if (op > OPC_D) return false;
+            ops[nops++] = (uint8_t)(kChars >> (8 * op));
+            const int mj = op != OPC_I, mi = op != OPC_D;
+            j -= mj;
+            i -= mi;
+            d -= 1;
+            o.consumed += mi;
+            o.tcons += mj;
+            o.wcost += 1;
+            continue;
         }
         if (i < 0 || o.consumed >= budget) return true;
         if (j == 0) continue;

@@ -20,14 +20,16 @@ struct HostBand {
 };
 
 struct HostFull {
-    std::vector<uint64_t> w;  // [level][column]
-    int W = 0;
-    void reset(int levels, int W_) {
-        W = W_;
-        w.assign((size_t)levels * (W + 1), 0x5555aaaa5555aaaaull);
+    std::vector<uint64_t> w;  // [column][level]
+    int LV = 0;
+    void reset(int levels, int W) {
+        LV = levels;
+        w.assign((size_t)LV * (W + 1), 0x5555aaaa5555aaaaull);
     }
-    void put(int d, int j, uint64_t v) { w[(size_t)d * (W + 1) + j] = v; }
-    uint64_t get(int d, int j) const { return w[(size_t)d * (W + 1) + j]; }
+    void put4(int d0, int j, const uint32_t* lo, const uint32_t* hi) {
+        for (int k = 0; k < 4; ++k) w[(size_t)j * LV + d0 + k] = (uint64_t)hi[k] << 32 | lo[k];
+    }
+    uint64_t get(int d, int j) const { return w[(size_t)j * LV + d]; }
 };
 
 extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out,
@@ -37,6 +39,15 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
     const uint64_t lut = make_prio_lut(cfg->priority);
     HostBand band;
     HostFull full;
+    // the kernel's bit-plane form of the codes
+    const int64_t pw = (in->codes_len + 63) / 64 + 1;
+    std::vector<uint64_t> pl((size_t)pw * 3, 0);
+    for (int64_t x = 0; x < in->codes_len; ++x) {
+        const uint8_t c = in->codes[x];
+        pl[x >> 6] |= (uint64_t)(c & 1) << (x & 63);
+        pl[pw + (x >> 6)] |= (uint64_t)((c >> 1) & 1) << (x & 63);
+        pl[2 * pw + (x >> 6)] |= (uint64_t)((c >> 2) & 1) << (x & 63);
+    }
     for (int64_t q = 0; q < in->n_pairs; ++q) {
         ga_pair_result& r = out->results[q];
         memset(&r, 0, sizeof r);
@@ -69,12 +80,13 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                     break;
                 }
                 d_min = m;
-                Planes pp = load_planes(P + p, m), tp{0, 0, 0};
+                Planes pp = load_planes_bits(pl.data(), pw, in->pat_off[q] + p, m), tp{0, 0, 0};
                 ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, m, n, d_min,
                                budget, lut, ops, nops, o);
                 tier_counts[2]++;
             } else {
-                Planes pp = load_planes(P + p, m), tp = load_planes(T + t, n);
+                Planes pp = load_planes_bits(pl.data(), pw, in->pat_off[q] + p, m),
+                       tp = load_planes_bits(pl.data(), pw, in->txt_off[q] + t, n);
                 band.reset(n);
                 uint32_t okm = dc_band(pp, tp, m, n, band);
                 const int lim = K < 15 ? K : 15;
@@ -87,7 +99,7 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                     status = GA_WINDOW_FAILED;
                     break;
                 } else {
-                    full.reset(K + kPassLevels + 1, W);
+                    full.reset((K + kPassLevels) / kPassLevels * kPassLevels, W);
                     d_min = dc_full(pp, tp, m, n, K, full);
                     if (d_min < 0) {
                         status = GA_WINDOW_FAILED;
