@@ -276,9 +276,8 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     e = cudaMemsetAsync(sc->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
-    // W <= 64: the lane-per-pair kernel (which hands its outlier pairs to the
-    // lane-group kernel); GA_KERNEL=lockstep forces the lane-group kernel,
-    // which also serves W > 64
+    // W <= 64: the lane-per-pair kernel; GA_KERNEL=lockstep forces the
+    // lane-group kernel, which also serves W > 64
     const char* kern = getenv("GA_KERNEL");
     const bool lockstep = P.W > 64 || (kern && strcmp(kern, "lockstep") == 0);
     if (lockstep) {
@@ -287,8 +286,8 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
         e = genasm::launch_genasm_lockstep(P, group, block, c->num_sms, st, &sc->overflow,
                                            &sc->overflow_cap, &c->last_shape);
     } else {
-        e = genasm::launch_genasm_thread(P, c->num_sms, st, &sc->thr, &sc->thr_cap, &sc->overflow,
-                                         &sc->overflow_cap, &c->last_shape);
+        e = genasm::launch_genasm_thread(P, c->num_sms, st, &sc->thr, &sc->thr_cap,
+                                         &c->last_shape);
     }
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
     return 0;

@@ -70,16 +70,6 @@ struct KernelParams {
     int64_t overflow_words_per_group;
     uint32_t* band;            // per-warp global band tables
     unsigned long long* queue; // atomic pair counter
-    // lane-group kernel only: take the pair count from device memory and
-    // resume every pair from the state parked in its result record (the
-    // pairs the lane-per-pair kernel handed over)
-    const unsigned long long* n_dev;
-    int32_t resume;
-    int32_t full_only;     // every window starts with full-width rows (no band pass)
-    int32_t warps_per_sm;  // residency cap (0: GA_WARPS_PER_SM or the default)
-    // lane-per-pair kernel only: hand-over list (pair ids) and its length
-    int32_t* handoff;
-    unsigned long long* n_handoff;
 };
 
 struct PairResult {  // == ga_pair_result
@@ -98,11 +88,9 @@ cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_t
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,
                                    size_t* cap, LaunchShape* shape);
 
-// the lane-per-pair kernel (genasm_thread.cu), W <= 64.  Pairs with many
-// windows beyond its band tier are parked and listed in P.handoff /
-// P.n_handoff for the lane-group kernel (P.resume, P.n_dev) to finish.
+// the lane-per-pair kernel (genasm_thread.cu), W <= 64; launches the
+// bit-plane conversion of the codes first
 cudaError_t launch_genasm_thread(const KernelParams& P, int num_sms, cudaStream_t stream,
-                                 uint32_t** scratch, size_t* cap, uint32_t** lock_scratch,
-                                 size_t* lock_cap, LaunchShape* shape);
+                                 uint32_t** scratch, size_t* cap, LaunchShape* shape);
 
 }  // namespace genasm

@@ -63,7 +63,7 @@ genasm_kernel(const KernelParams P) {
     int64_t cost = 0, rows = 0, reads = 0, writes = 0, words = 0;
 
     // called by all G lanes of the group
-    const unsigned long long n_eff = P.n_dev ? *P.n_dev : (unsigned long long)P.n_pairs;
+    const unsigned long long n_eff = (unsigned long long)P.n_pairs;
 
     auto write_result = [&](int status, int fail_window) {
         if (status == 1 || status == 3) {  // windows the pair never completed read as 0
@@ -109,18 +109,6 @@ genasm_kernel(const KernelParams P) {
                     p = t = nops = 0;
                     widx = 0;
                     cost = rows = reads = writes = words = 0;
-                    if (P.resume) {  // continue from the parked state
-                        const PairResult& r = results[pair];
-                        widx = r.fail_window;
-                        p = (int64_t)widx * (W - O);
-                        t = r.text_consumed;
-                        nops = r.ops_len;
-                        cost = r.cost;
-                        rows = r.rows_computed;
-                        reads = r.entry_reads;
-                        writes = r.entry_writes;
-                        words = r.words_allocated;
-                    }
                     if (Lp <= 0) write_result(2, -1);  // EmptyPattern (window.py:87-88)
                     else phase = NEED_WINDOW;
                 }
@@ -180,7 +168,7 @@ genasm_kernel(const KernelParams P) {
                     }
                 }
                 pass = 0;
-                full = BAND && P.full_only;
+                full = false;
                 if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
                     if (m <= K) {
                         d_min = m;
@@ -409,8 +397,7 @@ static cudaError_t launch_t(const KernelParams& base, int block, int num_sms, cu
     // resident warps bound the band tables' L2 footprint (≈34 KB per warp at W=64,
     // G=4); measured best on config 3 with occupancy-limited residency (≈24 warps)
     const char* cap_env = getenv("GA_WARPS_PER_SM");
-    const int warps_cap = P.warps_per_sm > 0 ? P.warps_per_sm
-                          : cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 64;
+    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 64;
     const int bcap = warps_cap * 32 / block;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
     int grid = num_sms * per_sm;
@@ -453,11 +440,7 @@ static cudaError_t launch_nw(const KernelParams& P, int group, int block, int nu
         case 4: return launch_t<NW, 4, 4>(P, block, num_sms, stream, overflow, cap, shape);
         case 8: return launch_t<NW, 8, 2>(P, block, num_sms, stream, overflow, cap, shape);
         case 16: return launch_t<NW, 16, 1>(P, block, num_sms, stream, overflow, cap, shape);
-        // 32 lanes x 2 levels: 64 levels per pass, full-width rows only (the
-        // band table holds 16 levels) -- the latency-bound hand-over pairs
-        case 32:
-            if (!P.full_only) return cudaErrorInvalidValue;
-            return launch_t<NW, 32, 2>(P, block, num_sms, stream, overflow, cap, shape);
+
         default: return cudaErrorInvalidValue;
     }
 }

@@ -6,30 +6,29 @@
 // No shuffles or cross-lane waits on the hot loop: four 32-bit operations
 // per DC entry.
 //
-// Windows with d_min > 15 (a few percent at 10 % divergence) need the full
-// tier (full-width rows, 16-level passes).  A lane that meets one parks the
-// pair (state saved in its result record, id pushed on the warp's HARD stack
-// in shared memory) and takes another pair, so the warp's fast loop never
-// diverges into the slow path.  When 32 hard windows are parked (or nothing
-// else is left) the warp runs them together: active pairs are parked on the
-// RESUME stack, each lane runs one hard window, the pairs go back on RESUME,
-// and free lanes refill from RESUME before taking fresh pairs from the warp's
-// static share of the longest-first order (dealt round-robin across warps).  Parked pairs resume oldest first, and while pairs
-// wait the active ones rotate out every 8 windows: every pair of a warp
-// advances at the same pace, so the warp's pairs finish together.
+// Windows with d_min > 15 (a few percent at 10 % divergence) are computed by
+// the whole warp together, right after the band step that found them: lane q
+// owns level q (0..31) of full-width rows and the 32 lanes sweep the window
+// as a wavefront (n + 31 steps, one shuffle of R[q-1][j] per step), storing
+// the rows in the warp's table (further passes of 32 levels as k allows, lane
+// 0 reading the row lane 31 stored); the owner lane then traces back alone.
 //
-// Tables.  Band tier: per warp, [column][word quad][lane] x 16 B -- each
-// column's 16 levels are 8 paired words (genasm_thread.cuh), two coalesced
-// 16-byte stores per lane.  Full tier: per lane,
-// [level][column] x 8 B.  Both live in the context's scratch slab.
+// Fresh pairs come from the warp's static share of the longest-first order,
+// dealt round-robin across warps, with just enough warps that every lane
+// gets the same number of pairs (pairs are long sequential chains).
+//
+// Tables, per warp, in the context's scratch slab.  Band tier:
+// [column][word quad][lane] x 16 B -- each column's 16 levels are 8 paired
+// words (genasm_thread.cuh), two coalesced 16-byte stores per lane.  Full
+// tier (one window at a time, the same region): [column][level] x 8 B.
 #include "genasm_device.cuh"
 #include "genasm_thread.cuh"
 
 namespace genasm {
 
 #ifdef GA_THREAD_STATS
-// dev counters: band steps, active lanes summed over band steps, hard batches,
-// hard lanes summed over batches
+// dev counters: band steps, active lanes summed over band steps, full-tier
+// windows, -, clock cycles in band steps, in full-tier windows
 __device__ unsigned long long g_thread_stats[8];
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
@@ -38,11 +37,15 @@ __device__ unsigned long long g_thread_stats[8];
 
 namespace {
 
-constexpr int kTBlock = 128;           // threads per block
+constexpr int kTBlock = 128;  // threads per block
 constexpr int kWarps = kTBlock / 32;
-constexpr int kStack = 128;            // per-warp HARD / RESUME stack entries
-constexpr int kHandoff = 24;           // full-tier windows before a pair is handed over
+constexpr int kFullLevels = 32;  // full tier: one level per lane
 constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
+
+// full-tier table: [pass][column][level within the pass] (a pass is 16 KB)
+__device__ __forceinline__ int full_index(int d, int j) {
+    return (d >> 5) * (64 * kFullLevels) + (j - 1) * kFullLevels + (d & 31);
+}
 
 struct BandTab {
     uint4* base;  // this warp's region: [column][word quad][lane] x 16 B
@@ -59,33 +62,15 @@ struct BandTab {
     }
 };
 
-struct FullTab {
-    uint64_t* base;  // this lane's rows, [column 1..W][level 0..LV)
-    int LV;
-    __device__ __forceinline__ void put4(int d0, int j, const uint32_t* lo, const uint32_t* hi) {
-        uint4* p = reinterpret_cast<uint4*>(base + (size_t)(j - 1) * LV + d0);
-        p[0] = make_uint4(lo[0], hi[0], lo[1], hi[1]);
-        p[1] = make_uint4(lo[2], hi[2], lo[3], hi[3]);
-    }
-    __device__ __forceinline__ uint64_t get(int d, int j) const {
-        return base[(size_t)(j - 1) * LV + d];
-    }
-};
-
-// full-tier rows stored per column: levels 0..k rounded up to whole passes
-__host__ __device__ __forceinline__ int full_levels(int k) {
-    return (k + thr::kPassLevels) / thr::kPassLevels * thr::kPassLevels;
-}
-
 // per-lane pair state (between windows)
 struct Lane {
     int pair;  // -1: none
-    int Lp, Lt, widx, hardc;  // hardc: windows that needed the full tier
+    int Lp, Lt, widx;
     int64_t pat, txt, ops, dst;  // offsets
     int64_t t, nops, cost, rows, reads, writes, words;
 };
 
-__device__ __forceinline__ void open_pair(const KernelParams& P, Lane& L, int pair) {
+__device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int pair) {
     L.pair = pair;
     L.Lp = P.pat_len[pair];
     L.Lt = P.txt_len[pair];
@@ -93,41 +78,8 @@ __device__ __forceinline__ void open_pair(const KernelParams& P, Lane& L, int pa
     L.txt = P.txt_off[pair];
     L.ops = P.ops_off[pair];
     L.dst = P.win_off[pair];
-}
-
-__device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int pair) {
-    open_pair(P, L, pair);
     L.widx = 0;
-    L.hardc = 0;
     L.t = L.nops = L.cost = L.rows = L.reads = L.writes = L.words = 0;
-}
-
-// park: the running state goes into the pair's own result record
-__device__ __forceinline__ void park(const KernelParams& P, const Lane& L) {
-    PairResult* r = reinterpret_cast<PairResult*>(P.results) + L.pair;
-    r->status = -1 - L.hardc;
-    r->fail_window = L.widx;
-    r->cost = L.cost;
-    r->text_consumed = L.t;
-    r->rows_computed = L.rows;
-    r->ops_len = L.nops;
-    r->entry_reads = L.reads;
-    r->entry_writes = L.writes;
-    r->words_allocated = L.words;
-}
-
-__device__ __forceinline__ void unpark(const KernelParams& P, Lane& L, int pair) {
-    open_pair(P, L, pair);
-    const PairResult* r = reinterpret_cast<const PairResult*>(P.results) + pair;
-    L.hardc = -1 - r->status;
-    L.widx = r->fail_window;
-    L.cost = r->cost;
-    L.t = r->text_consumed;
-    L.rows = r->rows_computed;
-    L.nops = r->ops_len;
-    L.reads = r->entry_reads;
-    L.writes = r->entry_writes;
-    L.words = r->words_allocated;
 }
 
 __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
@@ -153,90 +105,226 @@ __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int statu
     L.pair = -1;
 }
 
-enum : int { WIN_NEXT = 0, WIN_HARD = 1 };
+// geometry of lane L's current window (window.py:96-101)
+struct Win {
+    int64_t p;
+    int m, n, budget;
+    bool fin;
+};
 
-// One window of lane L's pair.  FULL = false: band tier, returns WIN_HARD if
-// d_min > 15 (and k allows more); FULL = true: full tier.  On completion of
-// the pair (or failure) the result is written and L.pair = -1.
-template <bool FULL>
-__device__ __forceinline__ int run_window(const KernelParams& P, Lane& L, BandTab& bt, FullTab& ft) {
-    using namespace thr;
-    const int W = P.W, K = P.k;
-    const int64_t p = (int64_t)L.widx * (W - P.O);  // every earlier window consumed W-O
-    const int64_t rem = L.Lp - p;
-    const bool fin = rem <= W;
-    const int m = fin ? (int)rem : W;
+__device__ __forceinline__ Win window_of(const KernelParams& P, const Lane& L) {
+    Win w;
+    w.p = (int64_t)L.widx * (P.W - P.O);  // every earlier window consumed W-O
+    const int64_t rem = L.Lp - w.p;
+    w.fin = rem <= P.W;
+    w.m = w.fin ? (int)rem : P.W;
     const int64_t tl = L.Lt - L.t;
-    const int n = tl < W ? (int)(tl > 0 ? tl : 0) : W;
-    const int budget = fin ? m : W - P.O;
-    const Planes pp = load_planes_bits(P.planes, P.plane_words, L.pat + p, m);
-    Planes tp{0ull, 0ull, 0ull};
-    int d_min;
-    uint8_t* ops = P.ops + L.ops;
-    TbOut o;
-    bool ok;
-    if (n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
-        if (m > K) {
-            finish(P, L, 1);
-            return WIN_NEXT;
-        }
-        d_min = m;
-        ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, m, n, d_min, budget,
-                       P.prio_lut, ops, L.nops, o);
-    } else {
-        tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, n);
-        if (!FULL) {
-            uint32_t okm = dc_band(pp, tp, m, n, bt);
-            const int lim = K < 15 ? K : 15;
-            okm &= (2u << lim) - 1u;
-            if (!okm) {
-                if (K <= 15) {
-                    finish(P, L, 1);
-                    return WIN_NEXT;
-                }
-                return WIN_HARD;
-            }
-            d_min = __ffs(okm) - 1;
-            ok = tb_band(bt, pp, tp, m, n, d_min, budget, P.prio_lut, ops, L.nops, o);
-        } else {
-            d_min = dc_full(pp, tp, m, n, K, ft);
-            if (d_min < 0) {
-                finish(P, L, 1);
-                return WIN_NEXT;
-            }
-            ok = traceback([&](int e, int c, int x) { return full_bit(ft, e, c, x); }, pp, tp, m, n,
-                           d_min, budget, P.prio_lut, ops, L.nops, o);
-        }
-    }
-    if (!ok) {
-        finish(P, L, 3);
-        return WIN_NEXT;
-    }
-    const int64_t wr = window_writes(n, budget, K, d_min);
+    w.n = tl < P.W ? (int)(tl > 0 ? tl : 0) : P.W;
+    w.budget = w.fin ? w.m : P.W - P.O;
+    return w;
+}
+
+// book a finished window (dists, counters, cursors); ends the pair when its
+// pattern is consumed
+__device__ __forceinline__ void book(const KernelParams& P, Lane& L, const Win& w, int d_min,
+                                     const thr::TbOut& o) {
+    const int64_t wr = thr::window_writes(w.n, w.budget, P.k, d_min);
     P.dists[L.dst + L.widx] = (uint8_t)d_min;
     L.rows += d_min + 1;
     L.cost += o.wcost;
     L.reads += o.reads;
     L.writes += wr;
-    L.words += wr * ((m + 63) / 64);
+    L.words += wr * ((w.m + 63) / 64);
     L.t += o.tcons;
     ++L.widx;
-    if (p + o.consumed >= L.Lp) finish(P, L, 0);
+    if (w.p + o.consumed >= L.Lp) finish(P, L, 0);
+}
+
+enum : int { WIN_NEXT = 0, WIN_HARD = 1 };
+
+// One band-tier window of lane L's pair.  Returns WIN_HARD (state untouched)
+// if d_min > 15 and k allows more; otherwise books the window.
+__device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandTab& bt) {
+    using namespace thr;
+    const int K = P.k;
+    const Win w = window_of(P, L);
+    const Planes pp = load_planes_bits(P.planes, P.plane_words, L.pat + w.p, w.m);
+    uint8_t* ops = P.ops + L.ops;
+    TbOut o;
+    int d_min;
+    bool ok;
+    if (w.n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
+        if (w.m > K) {
+            finish(P, L, 1);
+            return WIN_NEXT;
+        }
+        d_min = w.m;
+        const Planes tp{0ull, 0ull, 0ull};
+        ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, w.m, 0, d_min,
+                       w.budget, P.prio_lut, ops, L.nops, o);
+    } else {
+        const Planes tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, w.n);
+        uint32_t okm = dc_band(pp, tp, w.m, w.n, bt);
+        const int lim = K < 15 ? K : 15;
+        okm &= (2u << lim) - 1u;
+        if (!okm) {
+            if (K <= 15) {
+                finish(P, L, 1);
+                return WIN_NEXT;
+            }
+            return WIN_HARD;
+        }
+        d_min = __ffs(okm) - 1;
+        ok = tb_band(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, L.nops, o);
+    }
+    if (!ok) {
+        finish(P, L, 3);
+        return WIN_NEXT;
+    }
+    book(P, L, w, d_min, o);
     return WIN_NEXT;
 }
 
-// One full-tier window of a parked pair.  Returns true if the pair goes back
-// on RESUME.
-__device__ __forceinline__ bool hard_window(const KernelParams& P, int pair, uint4* band, int lane,
-                                         uint64_t* full) {
-    Lane L;
-    unpark(P, L, pair);
-    BandTab bt{band, lane};
-    FullTab ft{full, full_levels(P.k)};
-    run_window<true>(P, L, bt, ft);
-    if (L.pair < 0) return false;
-    park(P, L);
-    return true;
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+    return (uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), src) << 32 | __shfl_sync(FULL, (uint32_t)v, src);
+}
+
+// Full tier, the whole warp on one window: lane q computes level d0+q of
+// full-width rows (distance.py:125-149, two 32-bit words) as a wavefront --
+// at step s it evaluates column j = s - q + 1, taking R[d-1][j] from lane
+// q-1 by shuffle (lane q-1 produced it the step before; lane 0 reads the row
+// lane 31 stored in the previous pass) -- and stores every row to
+// tab[full_index(d, j)].  Passes of 32 levels run until a level <= k has
+// R[d][n] bit m-1 active or the passes cover kmax.  Returns that d_min, or -1.
+__device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes& tp, int m, int n,
+                                       int K, int kmax, uint64_t* tab, int lane) {
+    using namespace thr;
+    const int q = lane;
+    const uint32_t p0l = (uint32_t)pp.b0, p0h = (uint32_t)(pp.b0 >> 32);
+    const uint32_t p1l = (uint32_t)pp.b1, p1h = (uint32_t)(pp.b1 >> 32);
+    const uint32_t pnl = (uint32_t)pp.bn, pnh = (uint32_t)(pp.bn >> 32);
+    for (int d0 = 0; d0 <= K && d0 <= kmax; d0 += kFullLevels) {
+        const int d = d0 + q;
+        uint64_t c = init_row64(m, d);                    // R[d][j-1]
+        uint64_t a = d > 0 ? init_row64(m, d - 1) : 0ull; // R[d-1][j-1]
+        uint32_t ol = 0, oh = 0;                          // this lane's last output
+        for (int s = 0; s < n + kFullLevels - 1; ++s) {
+            uint32_t bl = __shfl_up_sync(FULL, ol, 1), bh = __shfl_up_sync(FULL, oh, 1);
+            const int j = s - q + 1;
+            if (j >= 1 && j <= n) {
+                if (q == 0 && d0 > 0) {  // R[d0-1][j]: the previous pass's last level
+                    const uint64_t v = tab[full_index(d0 - 1, j)];
+                    bl = (uint32_t)v;
+                    bh = (uint32_t)(v >> 32);
+                }
+                const uint32_t s0 = bcast(tp.b0, j - 1), s1 = bcast(tp.b1, j - 1),
+                               sn = bcast(tp.bn, j - 1);
+                const uint32_t pml = (p0l ^ s0) | (p1l ^ s1) | pnl | sn;
+                const uint32_t pmh = (p0h ^ s0) | (p1h ^ s1) | pnh | sn;
+                const uint32_t cl = (uint32_t)c, ch = (uint32_t)(c >> 32);
+                const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
+                const uint32_t xl = cl << 1, xh = shl1_hi(cl, ch);
+                uint32_t nl, nh;
+                if (d == 0) {  // level 0: the match edge only
+                    nl = xl | pml;
+                    nh = xh | pmh;
+                } else {
+                    nl = and3(orand(xl, pml, al << 1), bl << 1, al);
+                    nh = and3(orand(xh, pmh, shl1_hi(al, ah)), shl1_hi(bl, bh), ah);
+                }
+                a = (uint64_t)bh << 32 | bl;
+                c = (uint64_t)nh << 32 | nl;
+                ol = nl;
+                oh = nh;
+                tab[full_index(d, j)] = c;
+            }
+        }
+        __syncwarp();  // rows are read by the next pass's lane 0 and by the traceback
+        const bool hit = d <= K && !((c >> (m - 1)) & 1ull);
+        const unsigned hm = __ballot_sync(FULL, hit);
+        if (hm) return d0 + __ffs(hm) - 1;
+    }
+    return -1;
+}
+
+// hand-over list: pairs whose windows exceed one full-tier pass; the warps
+// that run out of pairs finish them (tail of genasm_thread_kernel)
+struct HandList {
+    int32_t* list;      // pair ids by ticket, -1 until published
+    unsigned* count;    // tickets handed out to producers
+    unsigned* claim;    // tickets taken by consumers
+    unsigned* done;     // warps that finished their own pairs
+};
+
+__device__ __forceinline__ void hand_over(const KernelParams& P, Lane& L, const HandList& H) {
+    PairResult* r = reinterpret_cast<PairResult*>(P.results) + L.pair;
+    r->fail_window = L.widx;
+    r->cost = L.cost;
+    r->text_consumed = L.t;
+    r->rows_computed = L.rows;
+    r->ops_len = L.nops;
+    r->entry_reads = L.reads;
+    r->entry_writes = L.writes;
+    r->words_allocated = L.words;
+    const unsigned slot = atomicAdd(H.count, 1u);
+    __threadfence();  // the state is visible before the id
+    atomicExch(H.list + slot, L.pair);
+    L.pair = -1;
+}
+
+__device__ __forceinline__ void resume_pair(const KernelParams& P, Lane& L, int pair) {
+    fresh_pair(P, L, pair);
+    const PairResult* r = reinterpret_cast<const PairResult*>(P.results) + pair;
+    L.widx = r->fail_window;
+    L.cost = r->cost;
+    L.t = r->text_consumed;
+    L.rows = r->rows_computed;
+    L.nops = r->ops_len;
+    L.reads = r->entry_reads;
+    L.writes = r->entry_writes;
+    L.words = r->words_allocated;
+}
+
+// One full-tier window of the pair owned by lane `owner`, computed by the
+// whole warp; the owner traces back and books it.  Levels up to kmax; returns
+// true (owner's state untouched) if the window needs more.
+__device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int owner, int lane,
+                                            int kmax, uint64_t* ftab) {
+    const int Lp = __shfl_sync(FULL, L.Lp, owner), Lt = __shfl_sync(FULL, L.Lt, owner);
+    const int widx = __shfl_sync(FULL, L.widx, owner);
+    const int64_t pat = (int64_t)shfl64((uint64_t)L.pat, owner);
+    const int64_t txt = (int64_t)shfl64((uint64_t)L.txt, owner);
+    const int64_t tt = (int64_t)shfl64((uint64_t)L.t, owner);
+    Lane V;
+    V.Lp = Lp;
+    V.Lt = Lt;
+    V.widx = widx;
+    V.t = tt;
+    const Win w = window_of(P, V);
+    const thr::Planes pp = thr::load_planes_bits(P.planes, P.plane_words, pat + w.p, w.m);
+    const thr::Planes tp = thr::load_planes_bits(P.planes, P.plane_words, txt + tt, w.n);
+    __syncwarp();  // the band tables of this step are no longer read
+    int d_min;
+    if (w.n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
+        d_min = w.m <= P.k ? w.m : -1;
+    } else {
+        d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, lane);
+        if (d_min < 0 && P.k > kmax) return true;
+    }
+    if (lane == owner) {
+        if (d_min < 0) {
+            finish(P, L, 1);
+        } else {
+            thr::TbOut o;
+            const bool ok = thr::traceback(
+                [&](int e, int c, int x) { return (uint32_t)(ftab[full_index(e, c)] >> x) & 1u; },
+                pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, P.ops + L.ops, L.nops, o);
+            if (ok) book(P, L, w, d_min, o);
+            else finish(P, L, 3);
+        }
+    }
+    __syncwarp();  // the table is rewritten by the next full-tier window
+    return false;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -288,129 +376,100 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
 #endif
 
 __global__ void __launch_bounds__(kTBlock, GA_THREAD_MINB)
-genasm_thread_kernel(const KernelParams P, uint32_t* band_base, uint64_t* full_base,
-                     int64_t full_words_per_lane) {
-    __shared__ int s_hard[kWarps][kStack], s_res[kWarps][kStack];
-    __shared__ int s_nh[kWarps], s_rh[kWarps], s_rt[kWarps];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H) {
+    const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    BandTab bt{reinterpret_cast<uint4*>(band_base + gw * kBandWordsPerWarp), lane};
-    FullTab ft{full_base + (gw * 32 + lane) * full_words_per_lane, full_levels(P.k)};
-    int* hard = s_hard[wib];  // stack of parked hard windows
-    int* res = s_res[wib];    // FIFO ring of parked pairs ready to resume
-    if (lane == 0) s_nh[wib] = s_rh[wib] = s_rt[wib] = 0;
-    __syncwarp();
+    uint32_t* region = band_base + gw * kBandWordsPerWarp;
+    BandTab bt{reinterpret_cast<uint4*>(region), lane};
+    uint64_t* ftab = reinterpret_cast<uint64_t*>(region);  // full tier reuses the region
     const unsigned lt = lanemask_lt();
-    bool exhausted = false;
-    int steps = 0;
-    int64_t taken = 0;
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    bool exhausted = false;
+    int64_t taken = 0;
     Lane L;
     L.pair = -1;
     for (;;) {
-        // ---- free lanes take parked pairs first (oldest first), then fresh ones ----
+        // ---- free lanes take fresh pairs: this warp's round-robin share ----
         unsigned freem = __ballot_sync(FULL, L.pair < 0);
-        if (freem) {
-            const int rh = s_rh[wib], nr = s_rt[wib] - rh;
-            const int rank = __popc(freem & lt);
-            const int take = min(__popc(freem), nr);
-            if (L.pair < 0 && rank < take) unpark(P, L, res[(rh + rank) & (kStack - 1)]);
-            __syncwarp();
-            if (lane == 0) s_rh[wib] = rh + take;
-            freem = __ballot_sync(FULL, L.pair < 0);
-            if (freem && !exhausted) {
-                // fresh pairs: this warp's static share of the longest-first
-                // order, dealt round-robin (every warp gets the same work)
-                const int cnt = __popc(freem);
-                const int64_t k0 = taken;
-                taken += cnt;
-                if ((uint64_t)(gw + taken * nwarps) >= (uint64_t)P.n_pairs) exhausted = true;
-                if (L.pair < 0) {
-                    const uint64_t idx = (uint64_t)gw + (uint64_t)(k0 + __popc(freem & lt)) * nwarps;
-                    if (idx < (uint64_t)P.n_pairs) {
-                        const int pair = P.order ? P.order[idx] : (int)idx;
-                        fresh_pair(P, L, pair);
-                        if (L.Lp <= 0) finish(P, L, 2);  // EmptyPattern (window.py:87-88)
-                    }
+        if (freem && !exhausted) {
+            const int cnt = __popc(freem);
+            const int64_t k0 = taken;
+            taken += cnt;
+            if ((uint64_t)(gw + taken * nwarps) >= (uint64_t)P.n_pairs) exhausted = true;
+            if (L.pair < 0) {
+                const uint64_t idx = (uint64_t)gw + (uint64_t)(k0 + __popc(freem & lt)) * nwarps;
+                if (idx < (uint64_t)P.n_pairs) {
+                    fresh_pair(P, L, P.order ? P.order[idx] : (int)idx);
+                    if (L.Lp <= 0) finish(P, L, 2);  // EmptyPattern (window.py:87-88)
                 }
             }
         }
-        __syncwarp();
-        const int nh = s_nh[wib];
-        const int nr = s_rt[wib] - s_rh[wib];
         const unsigned active = __ballot_sync(FULL, L.pair >= 0);
-        if (!active && nh == 0 && nr == 0 && exhausted) break;
-        const int nact = __popc(active);
-
-        // parked hard windows run as a batch once 32 wait, or once at least
-        // half of the warp's pairs in flight are parked (lanes would idle);
-        // every 8 steps with pairs waiting, the active pairs also rotate out so
-        // that all pairs of the warp advance at the same pace (no long tail)
-        const bool batch = nh >= 32 || (nh > 0 && nh >= nact + nr);
-        const bool rotate = !batch && nr > 0 && nact > 0 && (++steps & 7) == 0;
-        if (batch || rotate) {
-            int rt = s_rt[wib];
-            if (L.pair >= 0) {
-                park(P, L);
-                res[(rt + __popc(active & lt)) & (kStack - 1)] = L.pair;
-                L.pair = -1;
-            }
-            rt += nact;
-            int take = 0;
-            if (batch) {
-                // ---- hard batch: up to 32 full-tier windows, one per lane ----
-                take = nh < 32 ? nh : 32;
-                GA_STAT(2, 1);
-                GA_STAT(3, take);
-                int hp = -1;
-                if (lane < take) {
-                    hp = hard[nh - 1 - lane];
-                    if (!hard_window(P, hp, bt.base, lane, ft.base)) hp = -1;
-                }
-                const unsigned back = __ballot_sync(FULL, hp >= 0);
-                if (hp >= 0) res[(rt + __popc(back & lt)) & (kStack - 1)] = hp;
-                rt += __popc(back);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                s_rt[wib] = rt;
-                s_nh[wib] = nh - take;
-            }
-            __syncwarp();
+        if (!active) {
+            if (exhausted) break;
             continue;
         }
-        if (!active) continue;
 
         // ---- one band-tier window per active lane ----
         GA_STAT(0, 1);
-        GA_STAT(1, nact);
+        GA_STAT(1, __popc(active));
+#ifdef GA_THREAD_STATS
+        const long long tw0 = clock64();
+#endif
         int r = WIN_NEXT;
-        if (L.pair >= 0) r = run_window<false>(P, L, bt, ft);
-        // a pair whose windows keep needing the full tier (e.g. unrelated
-        // sequences) goes to the lane-group kernel instead of the hard stack
-        if (r == WIN_HARD && ++L.hardc > kHandoff) {
-            park(P, L);
-            P.handoff[atomicAdd(P.n_handoff, 1ull)] = L.pair;
-            L.pair = -1;
-            r = WIN_NEXT;
+        if (L.pair >= 0) r = band_window(P, L, bt);
+        unsigned hm = __ballot_sync(FULL, r == WIN_HARD);
+#ifdef GA_THREAD_STATS
+        GA_STAT(4, clock64() - tw0);
+        const long long th0 = clock64();
+#endif
+        // ---- windows beyond the band tier: the warp computes each one together;
+        // a window beyond level 31 hands its pair over (below) ----
+        while (hm) {
+            const int owner = __ffs(hm) - 1;
+            hm &= hm - 1;
+            GA_STAT(2, 1);
+            if (coop_window(P, L, owner, lane, kFullLevels - 1, ftab) && lane == owner)
+                hand_over(P, L, H);
         }
-        const unsigned hm = __ballot_sync(FULL, r == WIN_HARD);
-        if (hm) {
-            if (r == WIN_HARD) {
-                park(P, L);
-                hard[nh + __popc(hm & lt)] = L.pair;
-                L.pair = -1;
+#ifdef GA_THREAD_STATS
+        GA_STAT(5, clock64() - th0);
+#endif
+    }
+
+    // ---- handed-over pairs: warps out of work take one each and finish it
+    // together, every window in the full tier (up to k) ----
+    __threadfence();
+    if (lane == 0) atomicAdd(H.done, 1u);
+    for (;;) {
+        unsigned ticket = 0;
+        if (lane == 0) ticket = atomicAdd(H.claim, 1u);
+        ticket = __shfl_sync(FULL, ticket, 0);
+        int pair = -1;
+        for (;;) {  // wait until the ticket is published, or no more can come
+            if (lane == 0) {
+                pair = *(volatile int32_t*)(H.list + ticket);
+                if (pair < 0 && *(volatile unsigned*)H.done == (unsigned)nwarps &&
+                    ticket >= *(volatile unsigned*)H.count)
+                    pair = -2;
             }
-            __syncwarp();
-            if (lane == 0) s_nh[wib] = nh + __popc(hm);
-            __syncwarp();
+            pair = __shfl_sync(FULL, pair, 0);
+            if (pair != -1) break;
+            __nanosleep(1000);
+        }
+        if (pair < 0) break;
+        __threadfence();
+        L.pair = -1;
+        if (lane == 0) resume_pair(P, L, pair);
+        while (__shfl_sync(FULL, L.pair, 0) >= 0) {
+            // lane 0 owns the pair; window_of() on lane 0's state drives all lanes
+            if (coop_window(P, L, 0, lane, 1 << 30, ftab)) break;  // cannot happen: kmax covers k
         }
     }
 }
 
 cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStream_t stream,
-                                 uint32_t** scratch, size_t* cap, uint32_t** lock_scratch,
-                                 size_t* lock_cap, LaunchShape* shape) {
+                                 uint32_t** scratch, size_t* cap, LaunchShape* shape) {
     if (base.W > 64) return cudaErrorInvalidValue;
     KernelParams P = base;
     int per_sm = 0;
@@ -429,17 +488,14 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     const int64_t lanes = (P.n_pairs + waves - 1) / (waves > 0 ? waves : 1);
     int grid = (int)((lanes + kTBlock - 1) / kTBlock);
     if (grid < 1) grid = 1;
-    // scratch: band tables | full-tier rows (W x levels x 8 B per lane) |
-    // hand-over list (n_pairs ids) | its counter
-    const int64_t full_words = (int64_t)full_levels(P.k) * P.W * 2;
+    // scratch: per-warp tables | bit-planes (one word per 64 symbols per
+    // plane, plus a word of slack)
     const size_t warps = (size_t)grid * kWarps;
     const size_t band_words = (warps * kBandWordsPerWarp + 63) & ~(size_t)63;
-    const size_t full_total = (warps * 32 * (size_t)full_words + 63) & ~(size_t)63;
-    const size_t list_words = ((size_t)P.n_pairs + 63) & ~(size_t)63;
-    // bit-planes: one word per 64 symbols per plane, plus one word of slack
     const int64_t pw = (P.codes_len + 63) / 64 + 1;
     const size_t plane_total = ((size_t)pw * 3 * 2 + 63) & ~(size_t)63;
-    const size_t need = band_words + full_total + list_words + 64 + plane_total;
+    const size_t list_words = ((size_t)P.n_pairs + 63 + 64) & ~(size_t)63;
+    const size_t need = band_words + plane_total + list_words;
     if (need > *cap || !*scratch) {
         if (*scratch) cudaFree(*scratch);
         *scratch = nullptr;
@@ -449,12 +505,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
         *cap = need;
     }
     uint32_t* band = *scratch;
-    uint64_t* full = reinterpret_cast<uint64_t*>(*scratch + band_words);
-    P.handoff = reinterpret_cast<int32_t*>(*scratch + band_words + full_total);
-    P.n_handoff = reinterpret_cast<unsigned long long*>(*scratch + band_words + full_total +
-                                                        list_words);
-    if ((e = cudaMemsetAsync(P.n_handoff, 0, sizeof(unsigned long long), stream))) return e;
-    uint64_t* planes = reinterpret_cast<uint64_t*>(*scratch + band_words + full_total + list_words + 64);
+    uint64_t* planes = reinterpret_cast<uint64_t*>(*scratch + band_words);
     P.planes = planes;
     P.plane_words = pw;
     {
@@ -463,30 +514,22 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
             P.codes, P.codes_len, planes, pw);
         if ((e = cudaGetLastError())) return e;
     }
-    genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, full, full_words / 2);
-    if ((e = cudaGetLastError())) return e;
-    // the handed-over pairs: lane-group kernel, resuming from the parked state
-    KernelParams R = P;
-    R.order = P.handoff;
-    R.n_dev = P.n_handoff;
-    R.resume = 1;
-    // latency-bound: 32-lane groups, 64 levels per pass, few warps per SM so a
-    // group's full-width rows stay in L1 for its traceback
-    R.full_only = P.W > 32;
-    const char* hg = getenv("GA_HANDOFF_GROUP");
-    const char* hw = getenv("GA_HANDOFF_WARPS");
-    R.warps_per_sm = hw && atoi(hw) > 0 ? atoi(hw) : 4;
-    LaunchShape ls{};
-    e = launch_genasm_lockstep(R, hg && atoi(hg) > 0 ? atoi(hg) : (R.full_only ? 32 : 8), 0,
-                               num_sms, stream, lock_scratch, lock_cap, &ls);
+    HandList H;
+    H.list = reinterpret_cast<int32_t*>(*scratch + band_words + plane_total);
+    H.count = reinterpret_cast<unsigned*>(H.list + (((size_t)P.n_pairs + 63) & ~(size_t)63));
+    H.claim = H.count + 1;
+    H.done = H.count + 2;
+    if ((e = cudaMemsetAsync(H.list, 0xff, (size_t)P.n_pairs * 4, stream))) return e;
+    if ((e = cudaMemsetAsync(H.count, 0, 3 * sizeof(unsigned), stream))) return e;
+    genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, H);
     shape->grid = grid;
     shape->block = kTBlock;
     shape->smem_bytes = 0;
     shape->group = 1;
     shape->blocks_per_sm = per_sm;
-    shape->overflow_words_per_group = full_words;
-    shape->launches = 3;
-    return e;
+    shape->overflow_words_per_group = 0;
+    shape->launches = 2;
+    return cudaGetLastError();
 }
 
 }  // namespace genasm

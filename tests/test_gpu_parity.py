@@ -253,9 +253,10 @@ def test_both_kernels_vs_oracle(gpu, oracle_mod, monkeypatch, kernel):
         assert got == exp, (kernel, (w, o, k, prio))
 
 
-def test_handoff_of_unrelated_pairs(gpu, oracle_mod):
-    """Pairs whose windows all exceed the band tier (unrelated sequences) are
-    handed from the lane-per-pair kernel to the lane-group kernel mid-pair."""
+def test_unrelated_pairs_full_tier(gpu, oracle_mod):
+    """Pairs whose windows all exceed the band tier (unrelated sequences, d_min
+    often above 31): the lane-per-pair kernel's cooperative full tier with
+    several 32-level passes."""
     from paper_2203_15561_b200._abi import PackedBatch
     from paper_2203_15561_b200.engine import run_packed
     rng = np.random.default_rng(12)
@@ -267,4 +268,4 @@ def test_handoff_of_unrelated_pairs(gpu, oracle_mod):
     batch = PackedBatch.from_pairs(pairs)
     got = run_packed(batch, 64, 24, 64, "MSID")
     exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
-    _packed_equal(got, exp, "handoff")
+    _packed_equal(got, exp, "full tier")
