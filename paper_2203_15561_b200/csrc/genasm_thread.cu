@@ -448,9 +448,12 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         int pair = -1;
         for (;;) {  // wait until the ticket is published, or no more can come
             if (lane == 0) {
-                pair = *(volatile int32_t*)(H.list + ticket);
-                if (pair < 0 && *(volatile unsigned*)H.done == (unsigned)nwarps &&
-                    ticket >= *(volatile unsigned*)H.count)
+                // a ticket below count names a slot that will be published; past
+                // it, wait for the producers -- all warps done means none come
+                const bool all_done = *(volatile unsigned*)H.done == (unsigned)nwarps;
+                if (ticket < *(volatile unsigned*)H.count)
+                    pair = *(volatile int32_t*)(H.list + ticket);
+                else if (all_done && ticket >= *(volatile unsigned*)H.count)
                     pair = -2;
             }
             pair = __shfl_sync(FULL, pair, 0);
