@@ -334,7 +334,7 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     // ---- chunk plan: consecutive pairs, pipelined over kSlots slots.  Chunking
     // needs output offsets that grow with the input index (the prefix-sum
     // layout every caller in this package uses); otherwise one chunk. ----
-    int chunks = env_int("GA_CHUNKS", (int)std::min<int64_t>(3, std::max<int64_t>(1, n / 12000)));
+    int chunks = env_int("GA_CHUNKS", (int)std::min<int64_t>(4, std::max<int64_t>(1, n / 12000)));
     if (chunks < 1) chunks = 1;
     if (chunks > n) chunks = (int)n;
     for (int64_t q = 1; q < n && chunks > 1; ++q)
