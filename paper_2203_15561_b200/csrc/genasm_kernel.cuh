@@ -1,41 +1,20 @@
-// genasm_kernel.cuh -- fused windowed GenASM-DC + GenASM-TB for sm_100a.
+// genasm_kernel.cuh -- launch interface of the fused windowed GenASM-DC +
+// GenASM-TB kernels for sm_100a.
 //
-// Work mapping.  A persistent grid; every warp holds 32/G pairs, one per GROUP
-// of G consecutive lanes (G = 8 by default).  Groups pull pairs from an atomic
-// queue (longest first) and walk the reference's sequential window chain
-// (pkg/src/bitalign/window.py:95-120).  The groups of a warp advance in
-// PASS ROUNDS: every round, every group runs one DC pass of its current
-// window in lock-step (no divergence on the hot loop); groups whose window
-// solved in that pass then trace back together, set up their next window (or
-// pull the next pair) and rejoin at the next round.
+//   genasm_thread.cu (default, W <= 64): one pair per lane, DC in 32-bit
+//     diagonal bands (genasm_thread.cuh), windows with d_min > 15 computed by
+//     the whole warp as a levels-as-lanes wavefront.  DESIGN.md section 2.
 //
-//   DC pass (pkg/src/bitalign/distance.py:97-150): a wavefront of G lanes that
-//     covers 16 levels; lane q owns LPL = 16/G consecutive levels and at step s
-//     evaluates column j = s-q+1 of all of them, column-major inside the lane.
-//     The first of its levels takes R[d-1][j] from lane q-1 by one warp
-//     shuffle (lane 0: the carry row of the previous pass, full-width rows of
-//     its last level).  Rows are NW x 32-bit registers (W <= 32 NW).  Early
-//     termination (key idea 2): the window's DC ends with the first pass
-//     holding a level whose column-n row has bit m-1 clear.  The table keeps
-//     one status row per entry -- the AND of the four edges (key idea 1).
-//
-//   Table (key idea 3, extended to bits).  A traceback state (d, j, i) on any
-//     path from (d_min, n, m-1) satisfies |(m-1-i) - (n-j)| <= d_min - d, so
-//     every table read of entry (e, j) touches bits within d_min - e of the
-//     diagonal c_j = m-1-n+j.  When d_min <= 15 a 32-bit band around c_j holds
-//     every bit the traceback can ever read: band mode stores 32 bits per entry
-//     for levels 0..15, in a per-warp global region laid out [pass][step][lane]
-//     x LPL words so each wavefront step is one coalesced 16-byte store per
-//     lane (the region stays L2-resident).  A window needing level 16+ restarts
-//     in full mode (full-width rows in a per-group global slab).  W <= 32 rows
-//     are 32 bits wide and need no band.
-//
-//   TB (pkg/src/bitalign/backtrace.py:70-167): greedy walk from
-//     (j=n, d=d_min, i=m-1), edge bits recomputed from three table reads and
-//     the symbol codes (backtrace.py:84-99), first active edge by a priority
-//     LUT.  The G lanes speculate G consecutive diagonal ('=') steps at once;
-//     a ballot finds the first non-match, so a run of matches costs one round
-//     trip.  Ops are emitted in walk (= forward) order.
+//   genasm_lockstep.cu (W > 64, or GA_KERNEL=lockstep): every group of G lanes
+//     owns one pair; the groups of a warp advance in PASS ROUNDS: each round,
+//     every group runs one DC pass of its current window in lock-step (a
+//     wavefront of G lanes x 16/G levels, R[d-1][j] passed by SHFL.UP), groups
+//     whose window solved trace back together (G diagonal steps speculated per
+//     ballot), set up their next window and rejoin.  A traceback state
+//     (d, j, i) on any path from (d_min, n, m-1) satisfies
+//     |(m-1-i) - (n-j)| <= d_min - d, so when d_min <= 15 a 32-bit band around
+//     the diagonal holds every bit the traceback reads: band words per warp in
+//     global memory, full-width rows in per-group slabs above level 15.
 //
 // Counters follow the reference's stored predicate (dptable.py:62-82) in
 // closed form; entry reads are counted per taken step.
