@@ -285,6 +285,90 @@ __device__ __forceinline__ void resume_pair(const KernelParams& P, Lane& L, int 
     L.words = r->words_allocated;
 }
 
+// Traceback of a full-tier window by the whole warp (backtrace.py:88-160):
+// lane q evaluates the state q diagonal ('=') steps ahead; the first lane
+// whose step is not '=' (ballot) ends the run and its step is taken, so a run
+// of up to 32 '=' costs one round of table reads.  The walk is warp-uniform;
+// the ops go to ops[nops..], counters to o.
+__device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& pp,
+                                        const thr::Planes& tp, int m, int n, int d_min, int budget,
+                                        uint64_t prio_lut, uint8_t* ops, int64_t& nops,
+                                        thr::TbOut& o, int lane) {
+    using namespace thr;
+    constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
+    auto bit = [&](int e, int c, int x) -> uint32_t {
+        return (uint32_t)(tab[full_index(e, c)] >> x) & 1u;
+    };
+    int d = d_min, j = n, i = m - 1;
+    o.consumed = o.tcons = o.wcost = 0;
+    o.reads = 0;
+    for (;;) {
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+            if (i + 1 > d) return false;
+            const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
+            for (int u = lane; u < take; u += 32) ops[nops + u] = 'I';
+            nops += take;
+            o.wcost += take;
+            o.consumed += take;
+            return true;
+        }
+        const int jq = j - lane, iq = i - lane;
+        int op = 4;  // this lane's state is past a limit: the run stops here
+        unsigned rd = 0;
+        if (iq >= 0 && o.consumed + lane < budget && jq >= 1) {
+            const bool symeq = !bit64(tp.bn, jq - 1) && !bit64(pp.bn, iq) &&
+                               bit64(tp.b0, jq - 1) == bit64(pp.b0, iq) &&
+                               bit64(tp.b1, jq - 1) == bit64(pp.b1, iq);
+            const int dm1 = d > 0 ? d - 1 : 0;
+            uint32_t mb = 0, sb = 0, db, ib = 0;
+            if (jq == 1) {  // column 0 = init(m, .): bit x inactive iff x >= level
+                mb = iq - 1 >= d;
+                sb = iq - 1 >= d - 1;
+                db = iq >= d - 1;
+            } else {
+                if (iq >= 1) {
+                    mb = bit(d, jq - 1, iq - 1);
+                    sb = bit(dm1, jq - 1, iq - 1);
+                }
+                db = bit(dm1, jq - 1, iq);
+            }
+            if (iq >= 1) ib = bit(dm1, jq, iq - 1);
+            const bool dpos = d > 0;
+            const bool mok = symeq && (iq == 0 || !mb);
+            const bool sok = dpos && (iq == 0 || !sb);
+            const bool iok = dpos && (iq == 0 || !ib);
+            const bool dok = dpos && !db;
+            const unsigned okm =
+                (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+            op = (int)((prio_lut >> (4 * okm)) & 0xFu);
+            rd = (unsigned)(jq >= 2) + (dpos ? (unsigned)(jq >= 2) + 1u : 0u);
+        }
+        const unsigned nz = __ballot_sync(FULL, op != OPC_M);
+        const int f = nz ? __ffs(nz) - 1 : 32;
+        const int opf = __shfl_sync(FULL, op, f & 31);
+        const bool taken = f < 32 && opf <= OPC_D;  // lane f's step is taken too
+        if (lane < f) ops[nops + lane] = '=';
+        o.reads += __reduce_add_sync(FULL, (lane < f || (taken && lane == f)) ? rd : 0u);
+        j -= f;
+        i -= f;
+        o.consumed += f;
+        o.tcons += f;
+        nops += f;
+        if (f == 32 || opf == 4) continue;
+        if (opf > OPC_D) return false;
+        if (lane == 0) ops[nops] = (uint8_t)(kChars >> (8 * opf));
+        ++nops;
+        const int mj = opf != OPC_I, mi = opf != OPC_D;
+        j -= mj;
+        i -= mi;
+        d -= 1;
+        o.consumed += mi;
+        o.tcons += mj;
+        o.wcost += 1;
+    }
+}
+
 // One full-tier window of the pair owned by lane `owner`, computed by the
 // whole warp; the owner traces back and books it.  Levels up to kmax; returns
 // true (owner's state untouched) if the window needs more.
@@ -311,14 +395,17 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
         d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, lane);
         if (d_min < 0 && P.k > kmax) return true;
     }
-    if (lane == owner) {
-        if (d_min < 0) {
-            finish(P, L, 1);
-        } else {
-            thr::TbOut o;
-            const bool ok = thr::traceback(
-                [&](int e, int c, int x) { return (uint32_t)(ftab[full_index(e, c)] >> x) & 1u; },
-                pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, P.ops + L.ops, L.nops, o);
+    if (d_min < 0) {
+        if (lane == owner) finish(P, L, 1);
+    } else {
+        // the walk, by all lanes; the owner books it
+        int64_t nops = (int64_t)shfl64((uint64_t)L.nops, owner);
+        uint8_t* ops = P.ops + (int64_t)shfl64((uint64_t)L.ops, owner);
+        thr::TbOut o;
+        const bool ok = coop_tb(ftab, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, nops, o,
+                                lane);
+        if (lane == owner) {
+            L.nops = nops;
             if (ok) book(P, L, w, d_min, o);
             else finish(P, L, 3);
         }

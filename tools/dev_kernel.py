@@ -59,7 +59,8 @@ def main():
         st = st.astype(np.float64) / reps
         print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
               f"full-tier windows {st[2]:.0f} hand-overs {st[3]:.0f} "
-              f"cycles/band step {st[4] / max(st[0], 1):.0f} full-tier cycles/step {st[5] / max(st[0], 1):.0f}")
+              f"cycles/band step {st[4] / max(st[0], 1):.0f} full-tier cycles/step {st[5] / max(st[0], 1):.0f} "
+              f"per full-tier window: DC {st[6] / max(st[2], 1):.0f} TB {st[7] / max(st[2], 1):.0f}")
     print(f"config {cfg_id} n={n} ms/launch {[round(x, 2) for x in times]} "
           f"best {min(times):.2f} ({n / min(times) * 1e3 / 1e6:.3f} M aln/s) "
           f"status {np.bincount(r['status'], minlength=4).tolist()}", flush=True)
