@@ -82,11 +82,26 @@ __device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int p
     L.t = L.nops = L.cost = L.rows = L.reads = L.writes = L.words = 0;
 }
 
-__device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
+// a failed pair: its record and the window distances it never completed (0);
+// rare, kept out of line (no lane state escapes: plain values in)
+__device__ __noinline__ void fail_pair(const KernelParams& P, int pair, int status, int widx, int Lp,
+                                       int64_t dst) {
     PairResult r{};
     r.status = status;
-    r.fail_window = -1;
+    r.fail_window = status == 2 ? -1 : widx;
+    if (status != 2) {
+        const int64_t step = P.W - P.O;
+        const int64_t nwin = Lp <= P.W ? 1 : 1 + (Lp - P.W + step - 1) / step;
+        for (int64_t i = widx; i < nwin; ++i) P.dists[dst + i] = 0;
+    }
+    reinterpret_cast<PairResult*>(P.results)[pair] = r;
+}
+
+__device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
     if (status == 0) {
+        PairResult r;
+        r.status = 0;
+        r.fail_window = -1;
         r.cost = L.cost;
         r.text_consumed = L.t;
         r.rows_computed = L.rows;
@@ -94,14 +109,10 @@ __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int statu
         r.entry_reads = L.reads;
         r.entry_writes = L.writes;
         r.words_allocated = L.words;
-    } else if (status != 2) {
-        r.fail_window = L.widx;
-        // windows the pair never completed read as 0
-        const int64_t step = P.W - P.O;
-        const int64_t nwin = L.Lp <= P.W ? 1 : 1 + (L.Lp - P.W + step - 1) / step;
-        for (int64_t i = L.widx; i < nwin; ++i) P.dists[L.dst + i] = 0;
+        reinterpret_cast<PairResult*>(P.results)[L.pair] = r;
+    } else {
+        fail_pair(P, L.pair, status, L.widx, L.Lp, L.dst);
     }
-    reinterpret_cast<PairResult*>(P.results)[L.pair] = r;
     L.pair = -1;
 }
 
@@ -158,10 +169,16 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
             finish(P, L, 1);
             return WIN_NEXT;
         }
+        // the walk starts in column 0, whose zeros cover the m insertions
+        // (backtrace.py column-0 rule): budget-many 'I'
         d_min = w.m;
-        const Planes tp{0ull, 0ull, 0ull};
-        ok = traceback([&](int, int, int) -> uint32_t { return 1u; }, pp, tp, w.m, 0, d_min,
-                       w.budget, P.prio_lut, ops, L.nops, o);
+        const int take = w.m < w.budget ? w.m : w.budget;
+        for (int u = 0; u < take; ++u) ops[L.nops + u] = 'I';
+        L.nops += take;
+        o.consumed = o.wcost = take;
+        o.tcons = 0;
+        o.reads = 0;
+        ok = true;
     } else {
         const Planes tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, w.n);
         uint32_t okm = dc_band(pp, tp, w.m, w.n, bt);
