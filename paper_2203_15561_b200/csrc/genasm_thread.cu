@@ -13,9 +13,9 @@
 // the rows in the warp's table (further passes of 32 levels as k allows, lane
 // 0 reading the row lane 31 stored); the owner lane then traces back alone.
 //
-// Fresh pairs come from the warp's static share of the longest-first order,
-// dealt round-robin across warps, with just enough warps that every lane
-// gets the same number of pairs (pairs are long sequential chains).
+// Fresh pairs come from a global longest-first queue, the grid fills every SM
+// equally.  A pair with 4 consecutive windows beyond the band tier is handed
+// over and finished by the warps that run out of pairs.
 //
 // Tables, per warp, in the context's scratch slab.  Band tier:
 // [column][word quad][lane] x 16 B -- each column's 16 levels are 8 paired
@@ -37,9 +37,13 @@ __device__ unsigned long long g_thread_stats[8];
 
 namespace {
 
-constexpr int kTBlock = 128;  // threads per block
+#ifndef GA_TBLOCK
+#define GA_TBLOCK 128
+#endif
+constexpr int kTBlock = GA_TBLOCK;  // threads per block
 constexpr int kWarps = kTBlock / 32;
 constexpr int kFullLevels = 32;  // full tier: one level per lane
+constexpr int kStreak = 4;       // consecutive full-tier windows before a hand-over
 constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
 
 // full-tier table: [pass][column][level within the pass] (a pass is 16 KB)
@@ -66,6 +70,7 @@ struct BandTab {
 struct Lane {
     int pair;  // -1: none
     int Lp, Lt, widx;
+    int streak;  // consecutive windows beyond the band tier
     int64_t pat, txt, ops, dst;  // offsets
     int64_t t, nops, cost, rows, reads, writes, words;
 };
@@ -79,6 +84,7 @@ __device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int p
     L.ops = P.ops_off[pair];
     L.dst = P.win_off[pair];
     L.widx = 0;
+    L.streak = 0;
     L.t = L.nops = L.cost = L.rows = L.reads = L.writes = L.words = 0;
 }
 
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
 }
 
 #ifndef GA_THREAD_MINB
-#define GA_THREAD_MINB 4  // resident blocks per SM the register budget must allow
+#define GA_THREAD_MINB (512 / GA_TBLOCK)  // blocks per SM the register budget must allow
 #endif
 
 __global__ void __launch_bounds__(kTBlock, GA_THREAD_MINB)
@@ -489,19 +495,20 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     const unsigned lt = lanemask_lt();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     bool exhausted = false;
-    int64_t taken = 0;
     Lane L;
     L.pair = -1;
     for (;;) {
         // ---- free lanes take fresh pairs: this warp's round-robin share ----
         unsigned freem = __ballot_sync(FULL, L.pair < 0);
         if (freem && !exhausted) {
+            // fresh pairs from the global longest-first queue
             const int cnt = __popc(freem);
-            const int64_t k0 = taken;
-            taken += cnt;
-            if ((uint64_t)(gw + taken * nwarps) >= (uint64_t)P.n_pairs) exhausted = true;
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(P.queue, (unsigned long long)cnt);
+            base = __shfl_sync(FULL, base, 0);
+            if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
             if (L.pair < 0) {
-                const uint64_t idx = (uint64_t)gw + (uint64_t)(k0 + __popc(freem & lt)) * nwarps;
+                const uint64_t idx = base + __popc(freem & lt);
                 if (idx < (uint64_t)P.n_pairs) {
                     fresh_pair(P, L, P.order ? P.order[idx] : (int)idx);
                     if (L.Lp <= 0) finish(P, L, 2);  // EmptyPattern (window.py:87-88)
@@ -522,6 +529,16 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
 #endif
         int r = WIN_NEXT;
         if (L.pair >= 0) r = band_window(P, L, bt);
+        if (L.pair >= 0) {
+            // a pair whose windows keep leaving the band tier (unrelated or very
+            // divergent sequences) is handed over: the warps that run out of
+            // pairs finish it, so it does not hold its warp back
+            L.streak = r == WIN_HARD ? L.streak + 1 : 0;
+            if (L.streak >= kStreak) {
+                hand_over(P, L, H);
+                r = WIN_NEXT;
+            }
+        }
         unsigned hm = __ballot_sync(FULL, r == WIN_HARD);
 #ifdef GA_THREAD_STATS
         GA_STAT(4, clock64() - tw0);
@@ -541,6 +558,16 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
 #endif
     }
 
+#ifdef GA_THREAD_STATS
+    {  // spread of the warps' finishing times (global ns timer)
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        if (lane == 0) {
+            atomicMin(&g_thread_stats[6], tnow);
+            atomicMax(&g_thread_stats[7], tnow);
+        }
+    }
+#endif
     // ---- handed-over pairs: warps out of work take one each and finish it
     // together, every window in the full tier (up to k) ----
     __threadfence();
@@ -585,14 +612,13 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const char* cap_env = getenv("GA_WARPS_PER_SM");
-    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 16;
+    // 12 warps per SM measured best on config 3 (11-14 within 1 %)
+    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 12;
     const int bcap = warps_cap / kWarps;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
-    // pairs are long sequential chains, so give every lane the same number of
-    // pairs: the fewest waves the resident lanes allow, then just enough warps
+    // every SM equally loaded; lanes pull pairs from the global queue
     const int64_t resident = (int64_t)num_sms * per_sm * kTBlock;
-    const int64_t waves = (P.n_pairs + resident - 1) / resident;
-    const int64_t lanes = (P.n_pairs + waves - 1) / (waves > 0 ? waves : 1);
+    const int64_t lanes = P.n_pairs < resident ? P.n_pairs : resident;
     int grid = (int)((lanes + kTBlock - 1) / kTBlock);
     if (grid < 1) grid = 1;
     // scratch: per-warp tables | bit-planes (one word per 64 symbols per
@@ -645,7 +671,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
     cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 8);
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, ~0ull, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
     }
 }

@@ -41,9 +41,15 @@ def main():
                          d[2].data_ptr(), d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr())
     dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
                            d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
+    if hasattr(L, "ga_debug_thread_stats"):
+        z = np.zeros(8, np.uint64)
+        L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
     st = torch.cuda.Stream(dev)
     times = []
-    for _ in range(reps):
+    for it in range(reps):
+        if hasattr(L, "ga_debug_thread_stats") and it == reps - 1:
+            z = np.zeros(8, np.uint64)
+            L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         rc = L.ga_align_batch_device(ctx, C.byref(din), C.byref(cfg), C.byref(dout),
@@ -56,11 +62,11 @@ def main():
     if hasattr(L, "ga_debug_thread_stats"):
         st = np.zeros(8, np.uint64)
         L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
-        st = st.astype(np.float64) / reps
+        st = st.astype(np.float64)  # the last launch only
         print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
               f"full-tier windows {st[2]:.0f} hand-overs {st[3]:.0f} "
               f"cycles/band step {st[4] / max(st[0], 1):.0f} full-tier cycles/step {st[5] / max(st[0], 1):.0f} "
-              f"per full-tier window: DC {st[6] / max(st[2], 1):.0f} TB {st[7] / max(st[2], 1):.0f}")
+              f"warps finish own pairs over {(st[7] - st[6]) / 1e6:.2f} ms")
     print(f"config {cfg_id} n={n} ms/launch {[round(x, 2) for x in times]} "
           f"best {min(times):.2f} ({n / min(times) * 1e3 / 1e6:.3f} M aln/s) "
           f"status {np.bincount(r['status'], minlength=4).tolist()}", flush=True)
