@@ -270,6 +270,7 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     P.results = out->results;
     P.ops_off = out->ops_off;
     P.ops = out->ops;
+    P.ops_capacity = out->ops_capacity;
     P.win_off = out->win_off;
     P.dists = out->window_distances;
     P.queue = sc->queue;

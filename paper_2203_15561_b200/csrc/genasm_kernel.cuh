@@ -43,6 +43,7 @@ struct KernelParams {
     void* results;             // ga_pair_result[n_pairs]
     const int64_t* ops_off;
     uint8_t* ops;
+    int64_t ops_capacity;
     const int64_t* win_off;
     uint8_t* dists;
     uint32_t* overflow;        // per-group global full-mode table slabs

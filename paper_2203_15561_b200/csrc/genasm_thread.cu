@@ -198,7 +198,14 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
             return WIN_HARD;
         }
         d_min = __ffs(okm) - 1;
-        ok = tb_band(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, L.nops, o);
+#ifdef GA_DEV_TB_TWICE  // timing experiment: the traceback's cost, measured by doing it twice
+        {
+            int64_t nops2 = L.nops;
+            TbOut o2;
+            tb_band(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, nops2, o2);
+        }
+#endif
+        ok = tb_band<false>(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, L.nops, o);
     }
     if (!ok) {
         finish(P, L, 3);
@@ -371,7 +378,7 @@ __device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& 
         const int f = nz ? __ffs(nz) - 1 : 32;
         const int opf = __shfl_sync(FULL, op, f & 31);
         const bool taken = f < 32 && opf <= OPC_D;  // lane f's step is taken too
-        if (lane < f) ops[nops + lane] = '=';
+
         o.reads += __reduce_add_sync(FULL, (lane < f || (taken && lane == f)) ? rd : 0u);
         j -= f;
         i -= f;
@@ -653,6 +660,8 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     H.claim = H.count + 1;
     H.done = H.count + 2;
     if ((e = cudaMemsetAsync(H.list, 0xff, (size_t)P.n_pairs * 4, stream))) return e;
+    // the tracebacks write only the ops that are not '='
+    if ((e = cudaMemsetAsync(P.ops, '=', (size_t)P.ops_capacity, stream))) return e;
     if ((e = cudaMemsetAsync(H.count, 0, 3 * sizeof(unsigned), stream))) return e;
     genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, H);
     shape->grid = grid;

@@ -507,7 +507,9 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
 // bits read from the paired band words (positions relative to each column's
 // virtual band origin o_j) and the '=' test from the symbol planes.
 
-template <class Tab>
+// kWriteEq = false: the ops buffer was pre-filled with '=', only the other ops
+// are written
+template <bool kWriteEq = true, class Tab>
 GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
                    int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
     constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
@@ -565,7 +567,8 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             }
             okm &= (1u << K) - 1u;
             const int run = (int)ctz32(~okm);
-            for (int k = 0; k < run; ++k) ops[nops + k] = '=';
+            if (kWriteEq)
+                for (int k = 0; k < run; ++k) ops[nops + k] = '=';
             nops += run;
             j -= run;
             i -= run;
@@ -631,7 +634,8 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
         const int op = (int)((prio_lut >> (4 * okm)) & 0xFu);
         o.reads += (j >= 2) + (dpos ? (j >= 2) + 1 : 0);
         if (op > OPC_D) return false;
-        ops[nops++] = (uint8_t)(kChars >> (8 * op));
+        if (kWriteEq || op != OPC_M) ops[nops] = (uint8_t)(kChars >> (8 * op));
+        ++nops;
         const int mj = op != OPC_I;  // M, S, D consume a text symbol
         const int mi = op != OPC_D;  // M, S, I consume a pattern symbol
         const int md = op != OPC_M;
@@ -646,15 +650,15 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
 
 // entry_writes of one window in closed form (dptable.py:62-82, 156-171):
 // level d stores columns max(1, n - budget - (K - d) - 1) .. n
+// level dd stores min(n, c0 - dd) columns, c0 = budget + K + 2 (n >= 0,
+// dd <= d_min <= K): the first t = clamp(c0 - n + 1, 0, d_min + 1) levels store
+// all n, the rest c0 - dd
 GA_HD int64_t window_writes(int n, int budget, int K, int d_min) {
-    int64_t wr = 0;
-    for (int dd = 0; dd <= d_min; ++dd) {
-        int ss = n - budget - (K - dd) - 1;
-        ss = ss > 1 ? ss : 1;
-        const int cnt = n - ss + 1;
-        wr += cnt > 0 ? cnt : 0;
-    }
-    return wr;
+    const int64_t c0 = (int64_t)budget + K + 2;
+    int64_t t = c0 - n + 1;
+    t = t < 0 ? 0 : (t > d_min + 1 ? d_min + 1 : t);
+    const int64_t rest = d_min + 1 - t;  // levels t..d_min
+    return t * n + rest * c0 - ((int64_t)d_min * (d_min + 1) / 2 - t * (t - 1) / 2);
 }
 
 // first active edge in priority order for each 4-bit mask of active edges
