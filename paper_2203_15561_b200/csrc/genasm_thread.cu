@@ -46,9 +46,12 @@ constexpr int kFullLevels = 32;  // full tier: one level per lane
 constexpr int kStreak = 4;       // consecutive full-tier windows before a hand-over
 constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
 
-// full-tier table: [pass][column][level within the pass] (a pass is 16 KB)
+// full-tier table: [pass][wavefront step][level within the pass], 24 KB per
+// pass -- entry (d, j) was written at step j-1+(d mod 32) of its pass, so each
+// step's 32 rows are one coalesced 256-byte store
 __device__ __forceinline__ int full_index(int d, int j) {
-    return (d >> 5) * (64 * kFullLevels) + (j - 1) * kFullLevels + (d & 31);
+    const int e = d & 31;
+    return (d >> 5) * (96 * kFullLevels) + (j - 1 + e) * kFullLevels + e;
 }
 
 struct BandTab {
