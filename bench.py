@@ -360,6 +360,14 @@ def main():
     gcups = cells_all * args.steps / (total_ms_max * 1e-3) / 1e9
     bases_all = sum_over_ranks(float(work.pattern_bases))
 
+    traffic_gb = None  # from the committed ncu capture of this kernel on this workload
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "ncu_traffic.json")) as f:
+            traffic_gb = json.load(f)["dram_total_GB"]
+    except (OSError, ValueError, KeyError):
+        pass
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(batch, args.cpu_sample, 1, 0)
@@ -380,7 +388,9 @@ def main():
                        "parallelism": f"pair-sharded x{world}, no collective"},
             "gcups": gcups, "bases_per_s": bases_all * args.steps / (total_ms_max * 1e-3),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gop/s",
-                         "frac": achieved / peak if peak > 0 else None, "traffic": None,
+                         "frac": achieved / peak if peak > 0 else None,
+                         "traffic": traffic_gb, "traffic_unit": "GB of DRAM read+write per launch "
+                         "(ncu --set full capture, profiles/ncu_traffic.json)",
                          "ops_per_launch": work.alu_ops,
                          "definition": "5*sum_w (d_min+1)*n_w*ceil(m_w/32) int32 ops per launch "
                                        "/ mean CUDA-event launch time; peak = live LOP3+SHF "
