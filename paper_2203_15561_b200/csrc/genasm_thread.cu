@@ -230,12 +230,22 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
 // tab[full_index(d, j)].  Passes of 32 levels run until a level <= k has
 // R[d][n] bit m-1 active or the passes cover kmax.  Returns that d_min, or -1.
 __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes& tp, int m, int n,
-                                       int K, int kmax, uint64_t* tab, int lane) {
+                                       int K, int kmax, uint64_t* tab, uint2* pmt, int lane) {
     using namespace thr;
     const int q = lane;
-    const uint32_t p0l = (uint32_t)pp.b0, p0h = (uint32_t)(pp.b0 >> 32);
-    const uint32_t p1l = (uint32_t)pp.b1, p1h = (uint32_t)(pp.b1 >> 32);
-    const uint32_t pnl = (uint32_t)pp.bn, pnh = (uint32_t)(pp.bn >> 32);
+    {  // the window's full-width mismatch words, one per column, in shared memory
+        const uint32_t p0l = (uint32_t)pp.b0, p0h = (uint32_t)(pp.b0 >> 32);
+        const uint32_t p1l = (uint32_t)pp.b1, p1h = (uint32_t)(pp.b1 >> 32);
+        const uint32_t pnl = (uint32_t)pp.bn, pnh = (uint32_t)(pp.bn >> 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = q + 32 * h;  // column x+1
+            const uint32_t s0 = bcast(tp.b0, x), s1 = bcast(tp.b1, x), sn = bcast(tp.bn, x);
+            pmt[x] = make_uint2((p0l ^ s0) | (p1l ^ s1) | pnl | sn,
+                                (p0h ^ s0) | (p1h ^ s1) | pnh | sn);
+        }
+        __syncwarp();
+    }
     for (int d0 = 0; d0 <= K && d0 <= kmax; d0 += kFullLevels) {
         const int d = d0 + q;
         uint64_t c = init_row64(m, d);                    // R[d][j-1]
@@ -250,10 +260,8 @@ __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes&
                     bl = (uint32_t)v;
                     bh = (uint32_t)(v >> 32);
                 }
-                const uint32_t s0 = bcast(tp.b0, j - 1), s1 = bcast(tp.b1, j - 1),
-                               sn = bcast(tp.bn, j - 1);
-                const uint32_t pml = (p0l ^ s0) | (p1l ^ s1) | pnl | sn;
-                const uint32_t pmh = (p0h ^ s0) | (p1h ^ s1) | pnh | sn;
+                const uint2 pmv = pmt[j - 1];
+                const uint32_t pml = pmv.x, pmh = pmv.y;
                 const uint32_t cl = (uint32_t)c, ch = (uint32_t)(c >> 32);
                 const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
                 const uint32_t xl = cl << 1, xh = shl1_hi(cl, ch);
@@ -406,7 +414,7 @@ __device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& 
 // whole warp; the owner traces back and books it.  Levels up to kmax; returns
 // true (owner's state untouched) if the window needs more.
 __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int owner, int lane,
-                                            int kmax, uint64_t* ftab) {
+                                            int kmax, uint64_t* ftab, uint2* pmt) {
     const int Lp = __shfl_sync(FULL, L.Lp, owner), Lt = __shfl_sync(FULL, L.Lt, owner);
     const int widx = __shfl_sync(FULL, L.widx, owner);
     const int64_t pat = (int64_t)shfl64((uint64_t)L.pat, owner);
@@ -425,7 +433,7 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
     if (w.n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
         d_min = w.m <= P.k ? w.m : -1;
     } else {
-        d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, lane);
+        d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, pmt, lane);
         if (d_min < 0 && P.k > kmax) return true;
     }
     if (d_min < 0) {
@@ -502,6 +510,8 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     uint32_t* region = band_base + gw * kBandWordsPerWarp;
     BandTab bt{reinterpret_cast<uint4*>(region), lane};
     uint64_t* ftab = reinterpret_cast<uint64_t*>(region);  // full tier reuses the region
+    __shared__ uint2 s_pm[kWarps][64];  // full tier: mismatch words per column
+    uint2* pmt = s_pm[threadIdx.x >> 5];
     const unsigned lt = lanemask_lt();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     bool exhausted = false;
@@ -560,7 +570,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             const int owner = __ffs(hm) - 1;
             hm &= hm - 1;
             GA_STAT(2, 1);
-            if (coop_window(P, L, owner, lane, kFullLevels - 1, ftab) && lane == owner)
+            if (coop_window(P, L, owner, lane, kFullLevels - 1, ftab, pmt) && lane == owner)
                 hand_over(P, L, H);
         }
 #ifdef GA_THREAD_STATS
@@ -607,7 +617,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         if (lane == 0) resume_pair(P, L, pair);
         while (__shfl_sync(FULL, L.pair, 0) >= 0) {
             // lane 0 owns the pair; window_of() on lane 0's state drives all lanes
-            if (coop_window(P, L, 0, lane, 1 << 30, ftab)) break;  // cannot happen: kmax covers k
+            if (coop_window(P, L, 0, lane, 1 << 30, ftab, pmt)) break;  // cannot: kmax covers k
         }
     }
 }
