@@ -269,7 +269,7 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& ta
         tab.put(j, w);
     }
     // columns with o_j >= 1; four operations per entry
-#pragma unroll 2
+#pragma unroll 1
     for (int j = jA + 1; j <= n; ++j) {
         const int oj = o0 + j;
         const uint32_t pm = pm_word((uint32_t)(pp.b0 >> oj), (uint32_t)(pp.b1 >> oj),
