@@ -294,7 +294,6 @@ struct HandList {
     int32_t* list;      // pair ids by ticket, -1 until published
     unsigned* count;    // tickets handed out to producers
     unsigned* claim;    // tickets taken by consumers
-    unsigned* done;     // warps that finished their own pairs
 };
 
 __device__ __forceinline__ void hand_over(const KernelParams& P, Lane& L, const HandList& H) {
@@ -513,7 +512,6 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     __shared__ uint2 s_pm[kWarps][64];  // full tier: mismatch words per column
     uint2* pmt = s_pm[threadIdx.x >> 5];
     const unsigned lt = lanemask_lt();
-    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     bool exhausted = false;
     Lane L;
     L.pair = -1;
@@ -588,30 +586,33 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         }
     }
 #endif
-    // ---- handed-over pairs: warps out of work take one each and finish it
-    // together, every window in the full tier (up to k) ----
-    __threadfence();
-    if (lane == 0) atomicAdd(H.done, 1u);
+    // ---- handed-over pairs: a warp out of pairs claims the published ones,
+    // one at a time, and finishes each with all lanes, every window in the
+    // full tier (up to k).  It claims only while unclaimed tickets exist and
+    // then exits: every producer runs this loop after its own pairs, so no
+    // ticket is left behind and nobody waits for future hand-overs. ----
     for (;;) {
-        unsigned ticket = 0;
-        if (lane == 0) ticket = atomicAdd(H.claim, 1u);
-        ticket = __shfl_sync(FULL, ticket, 0);
-        int pair = -1;
-        for (;;) {  // wait until the ticket is published, or no more can come
-            if (lane == 0) {
-                // a ticket below count names a slot that will be published; past
-                // it, wait for the producers -- all warps done means none come
-                const bool all_done = *(volatile unsigned*)H.done == (unsigned)nwarps;
-                if (ticket < *(volatile unsigned*)H.count)
-                    pair = *(volatile int32_t*)(H.list + ticket);
-                else if (all_done && ticket >= *(volatile unsigned*)H.count)
-                    pair = -2;
+        int ticket = -1;
+        if (lane == 0) {
+            unsigned c = *(volatile unsigned*)H.claim;
+            while (c < *(volatile unsigned*)H.count) {
+                const unsigned prev = atomicCAS(H.claim, c, c + 1);
+                if (prev == c) {
+                    ticket = (int)c;
+                    break;
+                }
+                c = prev;
             }
-            pair = __shfl_sync(FULL, pair, 0);
-            if (pair != -1) break;
-            __nanosleep(1000);
         }
-        if (pair < 0) break;
+        ticket = __shfl_sync(FULL, ticket, 0);
+        if (ticket < 0) break;
+        int pair = -1;
+        for (;;) {  // the producer publishes right after taking the slot
+            if (lane == 0) pair = *(volatile int32_t*)(H.list + ticket);
+            pair = __shfl_sync(FULL, pair, 0);
+            if (pair >= 0) break;
+            __nanosleep(100);
+        }
         __threadfence();
         L.pair = -1;
         if (lane == 0) resume_pair(P, L, pair);
@@ -671,11 +672,10 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     H.list = reinterpret_cast<int32_t*>(*scratch + band_words + plane_total);
     H.count = reinterpret_cast<unsigned*>(H.list + (((size_t)P.n_pairs + 63) & ~(size_t)63));
     H.claim = H.count + 1;
-    H.done = H.count + 2;
     if ((e = cudaMemsetAsync(H.list, 0xff, (size_t)P.n_pairs * 4, stream))) return e;
     // the tracebacks write only the ops that are not '='
     if ((e = cudaMemsetAsync(P.ops, '=', (size_t)P.ops_capacity, stream))) return e;
-    if ((e = cudaMemsetAsync(H.count, 0, 3 * sizeof(unsigned), stream))) return e;
+    if ((e = cudaMemsetAsync(H.count, 0, 2 * sizeof(unsigned), stream))) return e;
     genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, H);
     shape->grid = grid;
     shape->block = kTBlock;
