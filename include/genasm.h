@@ -90,7 +90,9 @@ typedef struct {
     ga_pair_result* results;          /* n_pairs */
     const int64_t*  ops_off;          /* n_pairs, in ops */
     uint8_t*        ops;              /* ASCII '=','X','I','D' in walk (= forward) order,
-                                         or 2-bit op codes when ops2 != 0 */
+                                         or 2-bit op codes when ops2 != 0; the whole
+                                         capacity is written (bytes past a pair's
+                                         ops_len are unspecified) */
     int64_t         ops_capacity;     /* ops that fit in `ops` */
     const int64_t*  win_off;          /* n_pairs */
     uint8_t*        window_distances; /* AlignmentResult.window_distances, d_min per window;
