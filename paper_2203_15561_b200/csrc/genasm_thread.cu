@@ -190,7 +190,7 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
         ok = true;
     } else {
         const Planes tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, w.n);
-        uint32_t okm = dc_band(pp, tp, w.m, w.n, bt);
+        uint32_t okm = dc_band(pp, tp, w.m, w.n, band_jstore(w.n, w.budget), bt);
         const int lim = K < 15 ? K : 15;
         okm &= (2u << lim) - 1u;
         if (!okm) {

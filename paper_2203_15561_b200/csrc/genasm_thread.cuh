@@ -236,10 +236,12 @@ GA_HD uint32_t shl1_or(uint32_t b, uint32_t f) {
 // serves every column -- only the I-edge fill differs (the bit below the band
 // is virtual, 0, while o_j <= 0 and an out-of-band 1 after) and the mismatch
 // word is masked to real bits.  col[] ends as R[d][n]; tab.put(j, w) receives
-// each column's 8 paired words.  Returns the mask of levels d <= 15 with
-// R[d][n] bit m-1 active.
+// each column's 8 paired words -- from column jstore on: the traceback of a
+// window with d_min <= 15 never reads a column below n - budget - 15 (it
+// consumes at most budget-1 pattern and d_min deletion steps before its last
+// step).  Returns the mask of levels d <= 15 with R[d][n] bit m-1 active.
 template <class Tab>
-GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& tab) {
+GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, int jstore, Tab& tab) {
     uint32_t col[kFastLevels];
     const int o0 = m - n - 16;
 #pragma unroll
@@ -266,7 +268,7 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& ta
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
-        tab.put(j, w);
+        if (j >= jstore) tab.put(j, w);
     }
     // columns with o_j >= 1; four operations per entry
 #pragma unroll 1
@@ -287,7 +289,7 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, Tab& ta
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
-        tab.put(j, w);
+        if (j >= jstore) tab.put(j, w);
     }
     // success bit m-1 sits at band bit m-1-o_n = 15
     uint32_t ok = 0;
@@ -501,6 +503,12 @@ GA_HD bool traceback(BitFn&& BIT, const Planes& pp, const Planes& tp, int m, int
             return false;
         }
     }
+}
+
+// first table column the band-tier traceback can read (see dc_band)
+GA_HD int band_jstore(int n, int budget) {
+    const int j = n - budget - 15;
+    return j > 1 ? j : 1;
 }
 
 // Traceback of a band-tier window: the walk of traceback() with the level

@@ -88,7 +88,7 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                 Planes pp = load_planes_bits(pl.data(), pw, in->pat_off[q] + p, m),
                        tp = load_planes_bits(pl.data(), pw, in->txt_off[q] + t, n);
                 band.reset(n);
-                uint32_t okm = dc_band(pp, tp, m, n, band);
+                uint32_t okm = dc_band(pp, tp, m, n, band_jstore(n, budget), band);
                 const int lim = K < 15 ? K : 15;
                 okm &= (2u << lim) - 1u;
                 if (okm) {
