@@ -201,13 +201,6 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
             return WIN_HARD;
         }
         d_min = __ffs(okm) - 1;
-#ifdef GA_DEV_TB_TWICE  // timing experiment: the traceback's cost, measured by doing it twice
-        {
-            int64_t nops2 = L.nops;
-            TbOut o2;
-            tb_band(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, nops2, o2);
-        }
-#endif
         ok = tb_band<false>(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, L.nops, o);
     }
     if (!ok) {
