@@ -367,6 +367,17 @@ def main():
             traffic_gb = json.load(f)["dram_total_GB"]
     except (OSError, ValueError, KeyError):
         pass
+    hbm = None  # the same traffic against the driver-measured HBM copy bandwidth
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                               "MEASURED_PEAKS.json")) as f:
+            hbm_peak = float(json.load(f)["hbm_gbs"])
+        if traffic_gb:
+            got = traffic_gb / avg_launch_s
+            hbm = {"achieved": got, "peak": hbm_peak, "unit": "GB/s", "frac": got / hbm_peak,
+                   "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    except (OSError, ValueError, KeyError):
+        pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -404,7 +415,7 @@ def main():
                                      "path": "same call with ga_batch_in.packed2 (sequences "
                                              "held 2 bits/symbol on the host; packing not timed)"}},
             "gpu_launches": launches, "clocks": clock_info,
-            "extra": {"status_counts": status_counts, "windows": work.windows,
+            "extra": {"hbm": hbm, "status_counts": status_counts, "windows": work.windows,
                       "dc_entries": work.entries, "tb_steps": work.tb_steps,
                       "step_ms": [round(x, 3) for x in step_ms], "gen_s": round(gen_s, 2)},
         }
