@@ -52,7 +52,8 @@ typedef struct {
     int64_t        n_pairs;
     const uint8_t* codes;      /* symbol codes 0..4 (one byte per symbol), or 2-bit
                                   packed ACGT when packed2 != 0 */
-    int64_t        codes_len;  /* symbols in `codes` */
+    int64_t        codes_len;  /* symbols in `codes`; must cover every offset + length
+                                  (the device call converts exactly this range) */
     const int64_t* pat_off;    /* offsets and lengths are in symbols */
     const int32_t* pat_len;
     const int64_t* txt_off;
