@@ -269,3 +269,39 @@ def test_unrelated_pairs_full_tier(gpu, oracle_mod):
     got = run_packed(batch, 64, 24, 64, "MSID")
     exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
     _packed_equal(got, exp, "full tier")
+
+
+def test_device_call_vs_oracle(gpu, oracle_mod):
+    """ga_align_batch_device on torch-owned device buffers, asynchronous on a
+    caller stream (the bench's device-resident path), against the oracle."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2203_15561_b200 import _abi, engine, sim
+    batch, _ = sim.config_pairs(5, count=1200)
+    host = _abi.PackedResults.allocate(batch, 64, 24)
+    order = engine.lpt_order(batch.pat_len)
+    dev = torch.device("cuda:0")
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    d = [up(x) for x in (batch.codes, batch.pat_off, batch.pat_len, batch.txt_off, batch.txt_len,
+                         order, host.ops_off, host.win_off)]
+    res = torch.zeros(batch.n_pairs * 64, dtype=torch.uint8, device=dev)
+    ops = torch.zeros(host.ops.shape[0], dtype=torch.uint8, device=dev)
+    dst = torch.zeros(host.dists.shape[0], dtype=torch.uint8, device=dev)
+    din = _abi.GaBatchIn(batch.n_pairs, d[0].data_ptr(), int(batch.codes.shape[0]), d[1].data_ptr(),
+                         d[2].data_ptr(), d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr())
+    dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
+                           d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
+    stream = torch.cuda.Stream(dev)
+    L, ctx = engine.lib(), engine.context(0)
+    cfg = _abi.make_config(64, 24, 64, "MSID")
+    assert L.ga_align_batch_device(ctx, C.byref(din), C.byref(cfg), C.byref(dout),
+                                   C.c_void_p(stream.cuda_stream)) == 0
+    assert L.ga_last_launch_count(ctx) >= 1
+    stream.synchronize()
+    got = _abi.PackedResults(results=res.cpu().numpy().view(_abi.RESULT_DTYPE),
+                             ops_off=host.ops_off, ops=ops.cpu().numpy(), win_off=host.win_off,
+                             dists=dst.cpu().numpy(), n_ops=host.n_ops)
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    _packed_equal(got, exp, "device call")
