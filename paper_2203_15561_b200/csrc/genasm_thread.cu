@@ -67,6 +67,10 @@ struct BandTab {
                                                               (k >> 2) * 32 + lane);
         return p[k & 3];
     }
+    __device__ __forceinline__ int wi(int e) const { return thr::packed_word(e); }
+    __device__ __forceinline__ uint32_t bit(uint32_t w, int e, int b) const {
+        return thr::packed_bit(w, e, b);
+    }
 };
 
 // per-lane pair state (between windows)
@@ -509,10 +513,9 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     Lane L;
     L.pair = -1;
     for (;;) {
-        // ---- free lanes take fresh pairs: this warp's round-robin share ----
+        // ---- free lanes take fresh pairs from the global longest-first queue ----
         unsigned freem = __ballot_sync(FULL, L.pair < 0);
         if (freem && !exhausted) {
-            // fresh pairs from the global longest-first queue
             const int cnt = __popc(freem);
             unsigned long long base = 0;
             if (lane == 0) base = atomicAdd(P.queue, (unsigned long long)cnt);

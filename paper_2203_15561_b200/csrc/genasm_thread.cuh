@@ -512,8 +512,9 @@ GA_HD int band_jstore(int n, int budget) {
 }
 
 // Traceback of a band-tier window: the walk of traceback() with the level
-// bits read from the paired band words (positions relative to each column's
-// virtual band origin o_j) and the '=' test from the symbol planes.
+// bits read from the band table (tab.wi(e): the word of level e, tab.bit(w, e,
+// b): its bit at band position b, relative to each column's virtual band
+// origin o_j) and the '=' test from the symbol planes.
 
 // kWriteEq = false: the ops buffer was pre-filled with '=', only the other ops
 // are written
@@ -553,9 +554,9 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
                 eqv = diag_eq(pp, tp, sd);
             }
             const int u = i - (o0 + j);
-            const int kd = packed_word(d);
+            const int kd = tab.wi(d);
             const int dm1 = d > 0 ? d - 1 : 0;
-            const int ke = packed_word(dm1);
+            const int ke = tab.wi(dm1);
             // level d and d-1 words of columns j-1-k; level d-1 of column j too: the
             // step that ends the run reads from them as well
             uint32_t w[kRun], v[kRun];
@@ -571,7 +572,7 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
 #pragma unroll
             for (int k = 0; k < kRun; ++k) {
                 const uint32_t eq = (uint32_t)(eqv >> ((j - 1 - k) & 63)) & 1u;
-                okm |= (eq & ~packed_bit(w[k], d, u)) << k;
+                okm |= (eq & ~tab.bit(w[k], d, u)) << k;
             }
             okm &= (1u << K) - 1u;
             const int run = (int)ctz32(~okm);
@@ -593,9 +594,9 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
                 wp = run == k ? v[k - 1] : wp;
             }
             const bool dpos = d > 0;
-            const bool sok = dpos && !packed_bit(wr, dm1, u);
-            const bool iok = dpos && !packed_bit(wp, dm1, u - 1);
-            const bool dok = dpos && !packed_bit(wr, dm1, u + 1);
+            const bool sok = dpos && !tab.bit(wr, dm1, u);
+            const bool iok = dpos && !tab.bit(wp, dm1, u - 1);
+            const bool dok = dpos && !tab.bit(wr, dm1, u + 1);
             const unsigned om = (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
             const int op = (int)((prio_lut >> (4 * om)) & 0xFu);
             o.reads += dpos ? 3 : 1;
@@ -614,20 +615,20 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
         if (j == 0) continue;
         const int u = i - (o0 + j);  // band position of (i, j); (i-1, j-1) shares it
         const int dm1 = d > 0 ? d - 1 : 0;
-        const uint32_t wj = tab.get(packed_word(dm1), j);
+        const uint32_t wj = tab.get(tab.wi(dm1), j);
         uint32_t mb, sb, db;
         if (j >= 2) {
-            const uint32_t w1 = tab.get(packed_word(d), j - 1);
-            const uint32_t w2 = tab.get(packed_word(dm1), j - 1);
-            mb = packed_bit(w1, d, u);
-            sb = packed_bit(w2, dm1, u);
-            db = packed_bit(w2, dm1, u + 1);
+            const uint32_t w1 = tab.get(tab.wi(d), j - 1);
+            const uint32_t w2 = tab.get(tab.wi(dm1), j - 1);
+            mb = tab.bit(w1, d, u);
+            sb = tab.bit(w2, dm1, u);
+            db = tab.bit(w2, dm1, u + 1);
         } else {  // column 0 = init(m, .): bit x inactive iff x >= level
             mb = i - 1 >= d;
             sb = i - 1 >= d - 1;
             db = i >= d - 1;
         }
-        const uint32_t ib = packed_bit(wj, dm1, u - 1);
+        const uint32_t ib = tab.bit(wj, dm1, u - 1);
         const bool symeq = !bit64(tp.bn, j - 1) && !bit64(pp.bn, i) &&
                            bit64(tp.b0, j - 1) == bit64(pp.b0, i) &&
                            bit64(tp.b1, j - 1) == bit64(pp.b1, i);

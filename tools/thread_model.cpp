@@ -17,6 +17,8 @@ struct HostBand {
     void reset(int n) { w.assign((size_t)(n + 1) * 8, 0xdeadbeefu); }
     void put(int j, const uint32_t* pw) { memcpy(&w[(size_t)j * 8], pw, 32); }
     uint32_t get(int k, int c) const { return w[(size_t)c * 8 + k]; }
+    int wi(int e) const { return packed_word(e); }
+    uint32_t bit(uint32_t x, int e, int b) const { return packed_bit(x, e, b); }
 };
 
 struct HostFull {
