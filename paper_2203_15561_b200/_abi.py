@@ -43,6 +43,18 @@ class GaBatchOut(C.Structure):
                 ("ops2", C.c_int32)]
 
 
+class GaPairs(C.Structure):
+    """ga_pairs (include/genasm_io.h): a parsed pair-list TSV."""
+    _fields_ = [("n_pairs", C.c_int64), ("codes", C.c_void_p), ("codes_len", C.c_int64),
+                ("pat_off", C.c_void_p), ("pat_len", C.c_void_p), ("txt_off", C.c_void_p),
+                ("txt_len", C.c_void_p), ("ids", C.c_void_p), ("id_off", C.c_void_p),
+                ("impl", C.c_void_p)]
+
+
+GA_IO_OK, GA_IO_PARSE, GA_IO_NONASCII, GA_IO_NOMEM = 0, 1, 2, 3
+GA_ROWS_COLLAPSE_M, GA_ROWS_STATS = 1, 2
+
+
 # ga_pair_result, 64 bytes
 RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("fail_window", np.int32), ("cost", np.int64),
