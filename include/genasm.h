@@ -44,7 +44,10 @@ typedef struct {
     int32_t overlap;
     int32_t k;
     char    priority[4];
+    int32_t mode;      /* GA_MODE_IMPROVED (0) or GA_MODE_BASELINE (1): WindowConfig.mode */
 } ga_config;
+
+enum { GA_MODE_IMPROVED = 0, GA_MODE_BASELINE = 1 };
 
 /* A batch of (pattern, text) pairs: the `pairs` list of align_batch.
  * All sequences live in one code array; offsets index into it. */

@@ -42,9 +42,9 @@ def lib():
 
 
 def align_packed(batch: PackedBatch, window: int, overlap: int, k: int,
-                 priority: str = "MSID", threads: int = 1) -> PackedResults:
+                 priority: str = "MSID", threads: int = 1, mode: str = "improved") -> PackedResults:
     out = PackedResults.allocate(batch, window, overlap)
-    cfg = _abi.make_config(window, overlap, k, priority)
+    cfg = _abi.make_config(window, overlap, k, priority, mode)
     bin_ = batch.struct()
     bout = out.struct()
     rc = lib().oracle_align_batch(C.byref(bin_), C.byref(cfg), C.byref(bout), int(threads))
@@ -57,5 +57,5 @@ def align_batch(pairs, cfg, threads: int = 1):
     """Reference-shaped outcomes (list of BatchOutcome) computed by the oracle."""
     from paper_2203_15561_b200.window import outcomes_from_packed
     batch = PackedBatch.from_pairs(pairs)
-    out = align_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, threads)
+    out = align_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, threads, cfg.mode)
     return outcomes_from_packed(batch, out, cfg)

@@ -25,7 +25,7 @@ GA_MAX_WINDOW = 128
 
 class GaConfig(C.Structure):
     _fields_ = [("window", C.c_int32), ("overlap", C.c_int32), ("k", C.c_int32),
-                ("priority", C.c_char * 4)]
+                ("priority", C.c_char * 4), ("mode", C.c_int32)]
 
 
 class GaBatchIn(C.Structure):
@@ -212,5 +212,10 @@ class PackedResults:
         return tuple(self.dists[off:off + count].tolist())
 
 
-def make_config(window: int, overlap: int, k: int, priority: str) -> GaConfig:
-    return GaConfig(window, overlap, k, priority.encode("ascii"))
+GA_MODE_IMPROVED, GA_MODE_BASELINE = 0, 1
+MODE_IDS = {"improved": GA_MODE_IMPROVED, "baseline": GA_MODE_BASELINE}
+
+
+def make_config(window: int, overlap: int, k: int, priority: str,
+                mode: str = "improved") -> GaConfig:
+    return GaConfig(window, overlap, k, priority.encode("ascii"), MODE_IDS[mode])

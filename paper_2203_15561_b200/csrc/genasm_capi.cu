@@ -59,13 +59,17 @@ struct Scratch {
     size_t overflow_cap = 0;
     uint32_t* thr = nullptr;       // lane-per-pair kernel
     size_t thr_cap = 0;
+    uint64_t* dense = nullptr;     // unimproved engine: dense edge tables
+    size_t dense_cap = 0;
     void release() {
         if (overflow) cudaFree(overflow);
         if (thr) cudaFree(thr);
         if (queue) cudaFree(queue);
+        if (dense) cudaFree(dense);
         overflow = thr = nullptr;
         queue = nullptr;
-        overflow_cap = thr_cap = 0;
+        dense = nullptr;
+        overflow_cap = thr_cap = dense_cap = 0;
     }
 };
 
@@ -142,6 +146,10 @@ int ga_check_config(const ga_config* cfg, char* msg, int msg_len) {
         std::sort(t, t + 4);
         if (strcmp(t, "DIMS") != 0) {
             snprintf(buf, sizeof buf, "priority must be a permutation of 'MSID', got '%s'", s);
+            rc = 1;
+        } else if (cfg->mode != GA_MODE_IMPROVED && cfg->mode != GA_MODE_BASELINE) {
+            snprintf(buf, sizeof buf, "mode must be one of ('improved', 'baseline'), got %d",
+                     cfg->mode);
             rc = 1;
         } else if (W > GA_MAX_WINDOW) {
             snprintf(buf, sizeof buf, "window %d exceeds the kernel maximum of %d", W,
@@ -279,6 +287,12 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
     // W <= 64: the lane-per-pair kernel; GA_KERNEL=lockstep forces the
     // lane-group kernel, which also serves W > 64
+    if (cfg->mode == GA_MODE_BASELINE) {
+        e = genasm::launch_genasm_baseline(P, c->num_sms, st, &sc->dense, &sc->dense_cap,
+                                           &c->last_shape);
+        if (e != cudaSuccess) return fail(c, e, "genasm baseline kernel launch");
+        return 0;
+    }
     const char* kern = getenv("GA_KERNEL");
     const bool lockstep = P.W > 64 || (kern && strcmp(kern, "lockstep") == 0);
     if (lockstep) {

@@ -63,6 +63,11 @@ struct LaunchShape {
     int launches;  // kernels issued
 };
 
+// the unimproved engine (genasm_baseline.cu, mode="baseline"): all k+1 levels,
+// dense 4-edge tables, one warp per pair
+cudaError_t launch_genasm_baseline(KernelParams P, int num_sms, cudaStream_t stream,
+                                   uint64_t** scratch, size_t* cap, LaunchShape* shape);
+
 // the fused kernel (genasm_lockstep.cu); group in {4, 8, 16} lanes per pair
 cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_threads,
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,

@@ -124,15 +124,16 @@ def pack2(codes: np.ndarray) -> _abi.Packed2:
 
 def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: str,
                device: int | None = None, *, packed2: bool = False,
-               ops2: bool = False) -> PackedResults:
+               ops2: bool = False, mode: str = "improved") -> PackedResults:
     """One ga_align_batch call on one device (host buffers in and out).
-    packed2 / ops2 select the 2-bit transfer formats of include/genasm.h."""
+    packed2 / ops2 select the 2-bit transfer formats of include/genasm.h;
+    mode="baseline" runs the unimproved engine (dense edge tables)."""
     dev = _default_device() if device is None else int(device)
     ctx = context(dev)
     out = PackedResults.allocate(batch, window, overlap, ops2=ops2)
     if batch.n_pairs == 0:
         return out
-    cfg = _abi.make_config(window, overlap, k, priority)
+    cfg = _abi.make_config(window, overlap, k, priority, mode)
     packed = pack2(batch.codes) if packed2 else None  # must outlive the call
     bin_ = batch.struct(packed=packed)
     bout = out.struct()
@@ -184,10 +185,12 @@ def run_batch(batch: PackedBatch, cfg, devices=None) -> PackedResults:
     """align_batch on one or more devices; results always in input order."""
     if devices is None or (isinstance(devices, int) and devices <= 1):
         dev = None if devices is None else 0
-        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev)
+        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev,
+                          mode=cfg.mode)
     dev_list = list(range(devices)) if isinstance(devices, int) else [int(d) for d in devices]
     if len(dev_list) == 1:
-        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev_list[0])
+        return run_packed(batch, cfg.window, cfg.overlap, cfg.k, cfg.priority, dev_list[0],
+                          mode=cfg.mode)
     shards = split_lpt(batch.pat_len, cfg.window, cfg.overlap, len(dev_list))
     parts: list[PackedResults | None] = [None] * len(dev_list)
     errors: list[BaseException] = []
@@ -195,7 +198,7 @@ def run_batch(batch: PackedBatch, cfg, devices=None) -> PackedResults:
     def work(s: int) -> None:
         try:
             parts[s] = run_packed(_subset(batch, shards[s]), cfg.window, cfg.overlap, cfg.k,
-                                  cfg.priority, dev_list[s])
+                                  cfg.priority, dev_list[s], mode=cfg.mode)
         except BaseException as exc:  # re-raised on the caller's thread
             errors.append(exc)
 

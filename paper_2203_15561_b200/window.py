@@ -118,9 +118,6 @@ class BatchOutcome:
 
 
 def _require_gpu_config(cfg: WindowConfig) -> None:
-    if cfg.mode != "improved":
-        raise ValueError(
-            f"mode {cfg.mode!r} has no GPU path; only the improved engine is implemented")
     if cfg.window > _abi.GA_MAX_WINDOW:
         raise ValueError(
             f"window {cfg.window} exceeds the kernel maximum of {_abi.GA_MAX_WINDOW}")

@@ -50,8 +50,6 @@ def test_validation_messages_match_reference(reference):
 def test_errors_before_any_device_work():
     with pytest.raises(ga.EmptyPattern, match="pattern must not be empty"):
         ga.align("", "ACGT")
-    with pytest.raises(ValueError, match="no GPU path"):
-        ga.align("ACGT", "ACGT", ga.WindowConfig(mode="baseline"))
     with pytest.raises(ValueError, match="kernel maximum"):
         ga.align_batch([("ACGT", "ACGT")], ga.WindowConfig(window=129))
     e = ga.WindowFailed(3, 16)

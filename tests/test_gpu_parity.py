@@ -305,3 +305,34 @@ def test_device_call_vs_oracle(gpu, oracle_mod):
                              dists=dst.cpu().numpy(), n_ops=host.n_ops)
     exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
     _packed_equal(got, exp, "device call")
+
+
+def test_baseline_mode_vs_oracle(gpu, oracle_mod):
+    """mode="baseline": the unimproved engine (all k+1 levels, dense 4-edge
+    tables, traceback over stored edges) against the oracle field for field
+    -- ops, distances and its own counters -- and against the reference's
+    digests (tests/golden/baseline.json)."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    with open(os.path.join(os.path.dirname(__file__), "golden", "baseline.json")) as f:
+        gold = json.load(f)
+    cases = corpus.fuzz_cases(gold["seed"], gold["batches"], pairs_per_batch=gold["pairs_per_batch"],
+                              max_len=gold["max_len"])
+    for case, ((w, o, k, prio), pairs) in zip(gold["cases"], cases):
+        cfg = gpu.WindowConfig(window=w, overlap=o, k=k, priority=prio, mode="baseline")
+        got = [str(corpus.digest(x)) for x in gpu.align_batch(pairs, cfg)]
+        assert got == case["digests"], case["cfg"]
+    for cfg_id, count, (w, o, k, prio) in [(1, 2000, (64, 24, 64, "MSID")),
+                                           (5, 64, (128, 48, 64, "SMDI")),
+                                           (5, 64, (32, 12, 8, "IDSM"))]:
+        batch, _ = sim.config_pairs(cfg_id, count=count)
+        got = run_packed(batch, w, o, k, prio, mode="baseline")
+        exp = oracle_mod.align_packed(batch, w, o, k, prio, threads=os.cpu_count(), mode="baseline")
+        _packed_equal(got, exp, ("baseline", cfg_id, w, o, k, prio))
+    # same alignments as the improved engine, different counters
+    batch, _ = sim.config_pairs(1, count=500)
+    imp = run_packed(batch, 64, 24, 64, "MSID")
+    base = run_packed(batch, 64, 24, 64, "MSID", mode="baseline")
+    for f in ("status", "cost", "text_consumed", "ops_len"):
+        assert np.array_equal(imp.results[f], base.results[f]), f
+    assert (base.results["rows_computed"] > imp.results["rows_computed"]).all()

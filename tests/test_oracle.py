@@ -112,3 +112,41 @@ def test_live_differential_vs_reference(oracle_mod, reference):
         ref = ref_batch(pairs, RefConfig(window=w, overlap=o, k=k, priority=prio))
         got = oracle_mod.align_batch(pairs, _cfg(w, o, k, prio))
         assert [corpus.outcome_key(x) for x in got] == [corpus.outcome_key(x) for x in ref]
+
+
+def _baseline_gold():
+    with open(os.path.join(GOLD, "baseline.json")) as f:
+        return json.load(f)
+
+
+def _cfg1_pairs(count):
+    from paper_2203_15561_b200 import sim
+    batch, _ = sim.config_pairs(1, count=count)
+    return [(sim.codes_to_str(batch.codes[batch.pat_off[q]:batch.pat_off[q] + batch.pat_len[q]]),
+             sim.codes_to_str(batch.codes[batch.txt_off[q]:batch.txt_off[q] + batch.txt_len[q]]))
+            for q in range(batch.n_pairs)]
+
+
+def test_baseline_mode_golden(oracle_mod):
+    """The unimproved engine (dc_baseline + stored-edge traceback) against the
+    reference's mode="baseline" outcomes, counters included
+    (tests/golden/make_baseline_golden.py)."""
+    gold = _baseline_gold()
+    cases = corpus.fuzz_cases(gold["seed"], gold["batches"], pairs_per_batch=gold["pairs_per_batch"],
+                              max_len=gold["max_len"])
+    for case, ((w, o, k, prio), pairs) in zip(gold["cases"], cases):
+        cfg = WindowConfig(window=w, overlap=o, k=k, priority=prio, mode="baseline")
+        got = [str(corpus.digest(x)) for x in oracle_mod.align_batch(pairs, cfg, threads=4)]
+        assert got == case["digests"], case["cfg"]
+    cfg = WindowConfig(mode="baseline")
+    got = [str(corpus.digest(x)) for x in oracle_mod.align_batch(_cfg1_pairs(200), cfg, threads=4)]
+    assert got == gold["cfg1_first200"]
+
+
+def test_baseline_known_counters(oracle_mod):
+    """cli.json's --mode baseline --stats rows: rows_computed k+1 per window,
+    4(k+1)n writes, 1 read per level-0 step and 4 above."""
+    r = oracle_mod.align_batch([("ACGT", "AGGT")], WindowConfig(mode="baseline"))[0].result
+    assert (r.cigar, r.cost, r.rows_computed) == ("=X==", 1, 65)
+    assert (r.counters.entry_reads, r.counters.entry_writes, r.counters.words_allocated) == \
+        (10, 1040, 1040)

@@ -27,7 +27,7 @@ def main():
     n = batch.n_pairs
     L = engine.lib()
     ctx = engine.context(0)
-    cfg = _abi.make_config(64, 24, 64, "MSID")
+    cfg = _abi.make_config(64, 24, 64, "MSID", os.environ.get("GA_MODE", "improved"))
     host = _abi.PackedResults.allocate(batch, 64, 24)
     dev = torch.device("cuda:0")
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
