@@ -140,6 +140,17 @@ const char* ga_last_error(const ga_ctx* ctx);
 int ga_align_batch(ga_ctx* ctx, const ga_batch_in* in, const ga_config* cfg,
                    ga_batch_out* out);
 
+/* Levenshtein distances of n pairs on the device -- the ground truth of the
+ * `bench` accuracy columns: oracle.global_distance (semiglobal = 0) or
+ * oracle.semiglobal_distance (semiglobal = 1; free text prefix),
+ * pkg/src/bitalign/oracle.py:59-74.  in->codes holds symbol ids, one byte
+ * per character (equal ids match, whatever the value -- unlike the
+ * aligner's codes, where 4 never matches; see ga_pairs.syms in
+ * genasm_io.h); packed2 is not supported.  dist[q] = the distance, or -1
+ * for an empty pattern with semiglobal = 1 (the reference raises).
+ * Synchronous. */
+int ga_edit_distance(ga_ctx* ctx, const ga_batch_in* in, int32_t semiglobal, int64_t* dist);
+
 /* Same call over DEVICE-resident buffers (every pointer in `in` and `out`
  * is a device pointer on the context's device).  Asynchronous on
  * `stream` (a cudaStream_t; NULL = the context's own stream). */

@@ -42,16 +42,22 @@ typedef struct {
     const int32_t* txt_len;
     const char*    ids;     /* id bytes, concatenated */
     const int64_t* id_off;  /* n_pairs + 1 prefix sums into ids */
+    const uint8_t* syms;    /* GA_PARSE_SYMBOLS: one symbol id per character, same layout as
+                               codes; ids are a bijection of the upper-cased bytes (ACGT ->
+                               0..3, bytes 0..3 -> 'A','C','G','T', others unchanged), so equal
+                               ids <=> equal characters; NULL otherwise */
     void*          impl;    /* library-private */
 } ga_pairs;
+
+enum { GA_PARSE_SYMBOLS = 1 };
 
 /* Parse `id<TAB>pattern<TAB>text` rows from a buffer holding a whole file.
  * Universal newlines (\n, \r\n, \r); blank lines and lines whose first
  * non-whitespace character is '#' are skipped but counted for line numbers;
  * a row with other than 3 columns or an empty pattern is a GA_IO_PARSE error
  * reporting the first such line.  nthreads <= 0: all hardware threads. */
-int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, ga_pairs** out, char* err,
-                       int64_t err_cap);
+int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, int32_t flags,
+                       ga_pairs** out, char* err, int64_t err_cap);
 void ga_pairs_free(ga_pairs* pairs);
 
 /* Flags of ga_format_align_rows */
@@ -60,7 +66,7 @@ enum { GA_ROWS_COLLAPSE_M = 1, GA_ROWS_STATS = 2 };
 /* The stdout of `bitalign align` for n pairs (cli.py:104-118): per pair
  * `id\tcost\ttext_consumed\tcigar[\trows\treads\twrites\twords]\n`, or
  * `id\tERROR <error>\n` for a failed slot (window.py:144-149).  Ops as in
- * ga_batch_out (ASCII, or 2-bit when ops2 != 0).  Writes into buf and returns
+ * ga_batch_out: ASCII, or 2-bit when ops2 != 0.  Writes into buf and returns
  * the byte count, -1 if cap is too small (n * 200 + the id bytes + twice the
  * ops always suffice), -2 if a result carries status GA_STUCK (the reference
  * raises instead of writing a row). */

@@ -48,11 +48,12 @@ class GaPairs(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("codes", C.c_void_p), ("codes_len", C.c_int64),
                 ("pat_off", C.c_void_p), ("pat_len", C.c_void_p), ("txt_off", C.c_void_p),
                 ("txt_len", C.c_void_p), ("ids", C.c_void_p), ("id_off", C.c_void_p),
-                ("impl", C.c_void_p)]
+                ("syms", C.c_void_p), ("impl", C.c_void_p)]
 
 
 GA_IO_OK, GA_IO_PARSE, GA_IO_NONASCII, GA_IO_NOMEM = 0, 1, 2, 3
 GA_ROWS_COLLAPSE_M, GA_ROWS_STATS = 1, 2
+GA_PARSE_SYMBOLS = 1
 
 
 # ga_pair_result, 64 bytes

@@ -106,6 +106,9 @@ struct ga_ctx {
     int64_t launches = 0;
     Scratch scratch;  // ga_align_batch_device
     Slot slot[kSlots];
+    DevBuf dp_in, dp_meta, dp_out;  // ga_edit_distance
+    uint64_t* dp_slab = nullptr;
+    size_t dp_cap = 0;
     genasm::LaunchShape last_shape{};
 };
 
@@ -223,6 +226,8 @@ void ga_destroy(ga_ctx* c) {
     cudaDeviceSynchronize();
     for (Slot& sl : c->slot) sl.release();
     c->scratch.release();
+    for (DevBuf* b : {&c->dp_in, &c->dp_meta, &c->dp_out}) b->release();
+    if (c->dp_slab) cudaFree(c->dp_slab);
     for (cudaStream_t s : {c->stream, c->stream_in, c->stream_out})
         if (s) cudaStreamDestroy(s);
     delete c;
@@ -305,6 +310,51 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
                                          &c->last_shape);
     }
     if (e != cudaSuccess) return fail(c, e, "genasm kernel launch");
+    return 0;
+}
+
+int ga_edit_distance(ga_ctx* c, const ga_batch_in* in, int32_t semiglobal, int64_t* dist) {
+    if (!c) return -1;
+    const int64_t n = in->n_pairs;
+    c->launches = 0;
+    if (n <= 0) return 0;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
+    int max_words = 1;
+    for (int64_t q = 0; q < n; ++q) max_words = std::max(max_words, (in->pat_len[q] + 63) / 64);
+    const size_t syms = (size_t)std::max<int64_t>(in->codes_len, 1);
+    const size_t meta = (size_t)n * (8 + 4 + 8 + 4 + 4);
+    if ((e = c->dp_in.ensure(syms)) || (e = c->dp_meta.ensure(meta)) ||
+        (e = c->dp_out.ensure((size_t)n * 8)))
+        return fail(c, e, "cudaMalloc (edit distance)");
+    if (!c->scratch.queue && (e = cudaMalloc(&c->scratch.queue, sizeof(unsigned long long))))
+        return fail(c, e, "cudaMalloc");
+    char* m = (char*)c->dp_meta.ptr;
+    int64_t* pat_off = (int64_t*)m;
+    int64_t* txt_off = pat_off + n;
+    int32_t* pat_len = (int32_t*)(txt_off + n);
+    int32_t* txt_len = pat_len + n;
+    int32_t* order = txt_len + n;
+    std::vector<int32_t> ord((size_t)n);
+    if (in->order) std::copy(in->order, in->order + n, ord.begin());
+    else ga_lpt_order(n, in->pat_len, ord.data());  // longest first: no straggler at the end
+    cudaStream_t st = c->stream;
+    const struct { void* d; const void* h; size_t b; } cp[] = {
+        {c->dp_in.ptr, in->codes, (size_t)std::max<int64_t>(in->codes_len, 0)},
+        {pat_off, in->pat_off, (size_t)n * 8}, {txt_off, in->txt_off, (size_t)n * 8},
+        {pat_len, in->pat_len, (size_t)n * 4}, {txt_len, in->txt_len, (size_t)n * 4},
+        {order, ord.data(), (size_t)n * 4}};
+    for (const auto& x : cp)
+        if (x.b && (e = cudaMemcpyAsync(x.d, x.h, x.b, cudaMemcpyHostToDevice, st)))
+            return fail(c, e, "H2D (edit distance)");
+    e = genasm::launch_edit_distance((const uint8_t*)c->dp_in.ptr, pat_off, pat_len, txt_off, txt_len,
+                                     order, n, max_words, semiglobal, (int64_t*)c->dp_out.ptr,
+                                     c->num_sms, st, &c->dp_slab, &c->dp_cap, c->scratch.queue);
+    if (e != cudaSuccess) return fail(c, e, "edit distance kernel");
+    if ((e = cudaMemcpyAsync(dist, c->dp_out.ptr, (size_t)n * 8, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaStreamSynchronize(st)))
+        return fail(c, e, "edit distance");
+    c->launches = 1;
     return 0;
 }
 

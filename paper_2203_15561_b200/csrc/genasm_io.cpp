@@ -36,6 +36,20 @@ struct CodeLut {
 };
 const CodeLut kLut;
 
+// symbol ids: a bijection of the upper-cased bytes with ACGT at 0..3
+struct SymLut {
+    uint8_t v[256];
+    SymLut() {
+        for (int b = 0; b < 256; ++b) v[b] = (uint8_t)((b >= 'a' && b <= 'z') ? b - 32 : b);
+        const uint8_t acgt[4] = {'A', 'C', 'G', 'T'};
+        for (int c = 0; c < 4; ++c) {
+            v[c] = acgt[c];
+            v[acgt[c]] = v[acgt[c] + 32] = (uint8_t)c;
+        }
+    }
+};
+const SymLut kSym;
+
 struct Line {
     int64_t s, e;  // content [s, e), terminator excluded
     int64_t next;  // start of the next line
@@ -87,7 +101,7 @@ struct ChunkCount {
 
 struct PairsImpl {
     ga_pairs view{};
-    std::vector<uint8_t> codes;
+    std::vector<uint8_t> codes, syms;
     std::vector<int64_t> pat_off, txt_off, id_off;
     std::vector<int32_t> pat_len, txt_len;
     std::vector<char> ids;
@@ -122,8 +136,9 @@ void put_err(char* err, int64_t cap, const std::string& msg) {
 
 extern "C" {
 
-int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, ga_pairs** out, char* err,
-                       int64_t err_cap) {
+int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, int32_t flags,
+                       ga_pairs** out, char* err, int64_t err_cap) {
+    const bool want_syms = flags & GA_PARSE_SYMBOLS;
     *out = nullptr;
     if (len < 0) len = 0;
     int nt = resolve_threads(nthreads);
@@ -195,6 +210,7 @@ int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, ga_pairs** o
     const int64_t n = pair0[nt];
     try {
         P->codes.resize((size_t)std::max<int64_t>(sym0[nt], 1));
+        if (want_syms) P->syms.resize((size_t)std::max<int64_t>(sym0[nt], 1));
         P->pat_off.resize((size_t)n);
         P->txt_off.resize((size_t)n);
         P->pat_len.resize((size_t)n);
@@ -221,10 +237,16 @@ int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, ga_pairs** o
             P->pat_off[q] = sym;
             P->pat_len[q] = (int32_t)lp;
             for (int64_t x = 0; x < lp; ++x) codes[sym + x] = kLut.v[(unsigned char)data[r.t1 + 1 + x]];
+            if (want_syms)
+                for (int64_t x = 0; x < lp; ++x)
+                    P->syms[sym + x] = kSym.v[(unsigned char)data[r.t1 + 1 + x]];
             sym += lp;
             P->txt_off[q] = sym;
             P->txt_len[q] = (int32_t)lt;
             for (int64_t x = 0; x < lt; ++x) codes[sym + x] = kLut.v[(unsigned char)data[r.t2 + 1 + x]];
+            if (want_syms)
+                for (int64_t x = 0; x < lt; ++x)
+                    P->syms[sym + x] = kSym.v[(unsigned char)data[r.t2 + 1 + x]];
             sym += lt;
             ++q;
         }
@@ -240,6 +262,7 @@ int ga_parse_pairs_tsv(const char* data, int64_t len, int nthreads, ga_pairs** o
     v.txt_len = P->txt_len.data();
     v.ids = P->ids.data();
     v.id_off = P->id_off.data();
+    v.syms = want_syms ? P->syms.data() : nullptr;
     v.impl = P;
     *out = &P->view;
     return GA_IO_OK;

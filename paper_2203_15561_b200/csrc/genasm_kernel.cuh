@@ -68,6 +68,13 @@ struct LaunchShape {
 cudaError_t launch_genasm_baseline(KernelParams P, int num_sms, cudaStream_t stream,
                                    uint64_t** scratch, size_t* cap, LaunchShape* shape);
 
+// Levenshtein distances for the accuracy columns (genasm_dp.cu)
+cudaError_t launch_edit_distance(const uint8_t* syms, const int64_t* pat_off, const int32_t* pat_len,
+                                 const int64_t* txt_off, const int32_t* txt_len, const int32_t* order,
+                                 int64_t n_pairs, int max_words, int semiglobal, int64_t* dist,
+                                 int num_sms, cudaStream_t stream, uint64_t** slab, size_t* cap,
+                                 unsigned long long* queue);
+
 // the fused kernel (genasm_lockstep.cu); group in {4, 8, 16} lanes per pair
 cudaError_t launch_genasm_lockstep(const KernelParams& P, int group, int block_threads,
                                    int num_sms, cudaStream_t stream, uint32_t** overflow,

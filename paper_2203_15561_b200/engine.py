@@ -61,10 +61,11 @@ def lib():
             "ga_unpack_ops": ([C.c_void_p, C.c_int64, C.c_int64, C.c_void_p], None),
             "ga_host_alloc": ([C.c_int64], C.c_void_p),
             "ga_host_free": ([C.c_void_p], None),
-            "ga_parse_pairs_tsv": ([C.c_char_p, C.c_int64, C.c_int,
+            "ga_parse_pairs_tsv": ([C.c_char_p, C.c_int64, C.c_int, C.c_int32,
                                     C.POINTER(C.POINTER(_abi.GaPairs)), C.c_char_p, C.c_int64],
                                    C.c_int),
             "ga_pairs_free": ([C.POINTER(_abi.GaPairs)], None),
+            "ga_edit_distance": ([C.c_void_p, B, C.c_int32, C.c_void_p], C.c_int),
             "ga_format_align_rows": ([C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int,
                                       C.c_void_p, C.c_int64], C.c_int64),

@@ -208,6 +208,7 @@ class LoadedPairs:
     batch: PackedBatch
     ids: bytes            # concatenated UTF-8 ids
     id_off: np.ndarray    # int64, n_pairs + 1
+    syms: np.ndarray | None = None  # symbols=True: per-character ids (equal <=> same character)
 
     @property
     def n_pairs(self) -> int:
@@ -224,16 +225,20 @@ def _arr(ptr: int, n: int, dtype) -> np.ndarray:
     return np.frombuffer((C.c_char * (n * item)).from_address(ptr), dtype=dtype).copy()
 
 
-def parse_pairs_bytes(data: bytes, threads: int = 0) -> LoadedPairs:
-    """``read_pairs`` over a whole file image, natively (ASCII files)."""
+def parse_pairs_bytes(data: bytes, threads: int = 0, symbols: bool = False) -> LoadedPairs:
+    """``read_pairs`` over a whole file image, natively (ASCII files).
+    symbols=True also returns per-character symbol ids (for the DP oracle,
+    where equal characters match whatever they are)."""
     from .engine import lib
     L = lib()
     out = C.POINTER(_abi.GaPairs)()
     err = C.create_string_buffer(256)
-    rc = L.ga_parse_pairs_tsv(data, len(data), threads, C.byref(out), err, 256)
+    rc = L.ga_parse_pairs_tsv(data, len(data), threads, _abi.GA_PARSE_SYMBOLS if symbols else 0,
+                              C.byref(out), err, 256)
     if rc == _abi.GA_IO_NONASCII:
         import io as _stdio
-        return _from_records(read_pairs(_stdio.StringIO(data.decode("utf-8"), newline=None)))
+        return _from_records(read_pairs(_stdio.StringIO(data.decode("utf-8"), newline=None)),
+                             symbols)
     if rc == _abi.GA_IO_PARSE:
         msg = err.value.decode()
         head, _, rest = msg.partition(": ")
@@ -251,27 +256,41 @@ def parse_pairs_bytes(data: bytes, threads: int = 0) -> LoadedPairs:
                             txt_off=_arr(v.txt_off, n, np.int64), txt_len=_arr(v.txt_len, n, np.int32))
         id_off = _arr(v.id_off, n + 1, np.int64)
         ids = C.string_at(v.ids, int(id_off[-1])) if n else b""
+        syms = None
+        if symbols:
+            syms = _arr(v.syms, int(v.codes_len), np.uint8) if v.codes_len else np.zeros(1, np.uint8)
     finally:
         L.ga_pairs_free(out)
-    return LoadedPairs(batch=batch, ids=ids, id_off=id_off)
+    return LoadedPairs(batch=batch, ids=ids, id_off=id_off, syms=syms)
 
 
-def _from_records(recs: list[PairRecord]) -> LoadedPairs:
+def _from_records(recs: list[PairRecord], symbols: bool = False) -> LoadedPairs:
     enc = [r.id.encode("utf-8") for r in recs]
     id_off = np.zeros(len(recs) + 1, dtype=np.int64)
     if recs:
         np.cumsum([len(e) for e in enc], out=id_off[1:])
-    return LoadedPairs(batch=PackedBatch.from_pairs([(r.pattern, r.text) for r in recs]),
-                       ids=b"".join(enc), id_off=id_off)
+    batch = PackedBatch.from_pairs([(r.pattern, r.text) for r in recs])
+    syms = None
+    if symbols:  # ids by code point: ACGT 0..3, every other character its own id
+        table = {"A": 0, "C": 1, "G": 2, "T": 3}
+        seq = "".join(r.pattern + r.text for r in recs)
+        for ch in set(seq) - set(table):
+            table[ch] = len(table)
+        if len(table) > 256:
+            raise ValueError("more than 252 distinct non-ACGT characters: no symbol ids")
+        syms = np.fromiter((table[ch] for ch in seq), dtype=np.uint8, count=len(seq))
+        if syms.shape[0] == 0:
+            syms = np.zeros(1, np.uint8)
+    return LoadedPairs(batch=batch, ids=b"".join(enc), id_off=id_off, syms=syms)
 
 
-def load_pairs(path: str, threads: int = 0) -> LoadedPairs:
+def load_pairs(path: str, threads: int = 0, symbols: bool = False) -> LoadedPairs:
     """``read_pairs(open(path))`` into device-ready arrays.  Raises what the
     reference's loader raises: FileNotFoundError, PairParseError,
     UnicodeDecodeError."""
     with open(path, "rb") as fh:
         data = fh.read()
-    return parse_pairs_bytes(data, threads)
+    return parse_pairs_bytes(data, threads, symbols)
 
 
 def format_align_rows(pairs: LoadedPairs, out: PackedResults, k: int, collapse_m: bool = False,

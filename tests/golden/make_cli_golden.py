@@ -6,11 +6,13 @@ container (the checkout exists only here):
 
 Output (committed): tests/golden/cli.json with
     files   name -> TSV text fed to the CLI / the pair reader
-    runs    [{file, argv, code, out, err}]      reference stdout/stderr/exit code
+    runs    [{file, argv, code, out, err}]      `align`: reference stdout/stderr/exit code
+    bench_runs  the same for `bench` (timing columns differ by nature)
     pairs   name -> read_pairs result ([id, pattern, text] rows) or the error text
     cigars  [ops, format_cigar, format_classic_cigar]
     parse   [text, parse_cigar result or "CigarError: ..."]
     fasta   name -> [text, read_fasta records or error, write_fasta(records, width 7)]
+    dp      [pattern, text, global_distance, semiglobal_distance or null]
 """
 
 from __future__ import annotations
@@ -28,6 +30,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from bitalign import cli as rcli  # noqa: E402
 from bitalign import io as rio  # noqa: E402
+from bitalign import oracle as roracle  # noqa: E402
 
 
 def _random_pairs(seed: int, count: int, max_len: int, rate: float) -> str:
@@ -85,17 +88,35 @@ RUNS = [
 ]
 
 
-def _run(path: str, argv: list[str]) -> dict:
+BENCH_FILES = {
+    "bench_two": "q1\t" + "ACGTTGCA" * 16 + "\t" + "ACGTTGCA" * 16 + "\nq2\t" + "ACGTTGCA" * 16
+                 + "\t" + ("ACGTTGCA" * 16)[:64] + "T" + ("ACGTTGCA" * 16)[65:] + "\n",
+    "bench_one": "q1\t" + "ACGTTGCA" * 8 + "\t" + "ACGTTGCA" * 8 + "\n",
+    "bench_sweep": "q1\t" + "ACGT" * 32 + "\t" + "ACGT" * 32 + "\n",
+    "bench_n": "a\tACGTNNACGTTAGC\tACGTNNACGATAGC\nb\tNNNN\tNNNN\nc\tACGTACGTAC\tTTTT\n",
+}
+BENCH_RUNS = [
+    ("bench_two", []), ("bench_one", []), ("bench_sweep", ["--sweep-k", "16,32,64"]),
+    ("bench_n", ["--w", "8", "--o", "2"]), ("bench_n", ["--w", "8", "--o", "2", "--k", "2"]),
+    ("random", ["--w", "32", "--o", "12", "--sweep-k", "8,32", "--priority", "IDSM"]),
+    ("random", ["--oracle-cap", "20000"]), ("random", ["--oracle-cap", "0"]),
+    ("random_hi", ["--w", "48", "--o", "18", "--sweep-k", "12,48"]),
+    ("bench_one", ["--sweep-k", "a,b"]), ("bench_one", ["--sweep-k", "0"]),
+]
+
+
+def _run(path: str, argv: list[str], cmd: str = "align") -> dict:
     out, err = io.StringIO(), io.StringIO()
     with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
-        code = rcli.main(["align", "--pairs", path, *argv])
+        code = rcli.main([cmd, "--pairs", path, *argv])
     return {"code": code, "out": out.getvalue(), "err": err.getvalue()}
 
 
 def main() -> None:
-    res: dict = {"files": FILES, "runs": [], "pairs": {}, "cigars": [], "parse": [], "fasta": {}}
+    res: dict = {"files": {**FILES, **BENCH_FILES}, "runs": [], "bench_runs": [], "pairs": {},
+                 "cigars": [], "parse": [], "fasta": {}}
     with tempfile.TemporaryDirectory() as tmp:
-        for name, text in FILES.items():
+        for name, text in res["files"].items():
             path = os.path.join(tmp, name + ".tsv")
             with open(path, "w", encoding="utf-8", newline="") as fh:
                 fh.write(text)
@@ -108,6 +129,10 @@ def main() -> None:
             r = _run(os.path.join(tmp, name + ".tsv"), argv)
             r["err"] = r["err"].replace(tmp, "<tmp>")
             res["runs"].append({"file": name, "argv": argv, **r})
+        for name, argv in BENCH_RUNS:
+            r = _run(os.path.join(tmp, name + ".tsv"), argv, "bench")
+            r["err"] = r["err"].replace(tmp, "<tmp>")
+            res["bench_runs"].append({"file": name, "argv": argv, **r})
     for ops in ["", "=", "====XX=", "IIDD=X=X", "X" * 12 + "=" * 3 + "D"]:
         res["cigars"].append([ops, rio.format_cigar(ops), rio.format_classic_cigar(ops)])
     for text in ["", "2=1I", "10=2X3D", "3=0X", "=3", "3=Q4X", "3=4", "12", "3M", "x1=", "1=x",
@@ -132,6 +157,24 @@ def main() -> None:
                                   buf.getvalue()]
         except rio.MalformedFasta as exc:
             res["fasta"][name] = [text, f"MalformedFasta: {exc}", None]
+    rng = random.Random(99)
+    res["dp"] = []
+    for q in range(120):
+        alpha = rng.choice(["ACGT", "ACGT", "ACGTN", "ACGTNX#", "ACé"])
+        p = "".join(rng.choice(alpha) for _ in range(rng.choice([0, 1, 5, 63, 64, 65, 130, 700])
+                                                        if q % 4 else rng.randint(0, 300)))
+        if rng.random() < 0.6:
+            t = list(p)
+            for _ in range(rng.randint(0, max(1, len(p) // 5))):
+                if t and rng.random() < 0.5:
+                    del t[rng.randrange(len(t))]
+                else:
+                    t.insert(rng.randint(0, len(t)), rng.choice(alpha))
+            t = "".join(t)
+        else:
+            t = "".join(rng.choice(alpha) for _ in range(rng.randint(0, 300)))
+        res["dp"].append([p, t, roracle.global_distance(p, t),
+                          roracle.semiglobal_distance(p, t) if p else None])
     with open(os.path.join(HERE, "cli.json"), "w") as fh:
         json.dump(res, fh, indent=0)
     print("wrote", os.path.join(HERE, "cli.json"), len(res["runs"]), "runs")
