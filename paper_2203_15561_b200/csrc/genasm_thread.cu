@@ -630,7 +630,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const char* cap_env = getenv("GA_WARPS_PER_SM");
     // 12 warps per SM measured best on config 3 (11-14 within 1 %)
-    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 12;
+    const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 16;
     const int bcap = warps_cap / kWarps;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
     // every SM equally loaded; lanes pull pairs from the global queue

@@ -240,12 +240,80 @@ GA_HD uint32_t shl1_or(uint32_t b, uint32_t f) {
 // window with d_min <= 15 never reads a column below n - budget - 15 (it
 // consumes at most budget-1 pattern and d_min deletion steps before its last
 // step).  Returns the mask of levels d <= 15 with R[d][n] bit m-1 active.
+// one-bit rotations: the D and I edges of levels >= 1 (see dc_band)
+GA_HD uint32_t rotr1(uint32_t a) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(a, a, 1);
+#else
+    return (a >> 1) | (a << 31);
+#endif
+}
+GA_HD uint32_t rotl1(uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_l(b, b, 1);
+#else
+    return (b << 1) | (b >> 31);
+#endif
+}
+
+// one band-tier column: levels 0..7 in band coordinates, levels 8..15 rotated
+// by 16 (r7 carries R[7][j-1] rotated); w[] receives the 8 paired words
+GA_HD void band_column(uint32_t* col, uint32_t& r7, uint32_t pm, uint32_t* w) {
+    uint32_t a = col[0];
+    uint32_t b = a | pm;  // level 0: the match edge only
+    col[0] = b;
+#pragma unroll
+    for (int d = 1; d < 8; ++d) {
+        const uint32_t c = col[d];
+        const uint32_t nc = and3(orand(c, pm, a), rotr1(a), rotl1(b));
+        a = c;
+        col[d] = nc;
+        b = nc;
+    }
+    const uint32_t pmr = rot16(pm);
+    a = r7;
+    b = rot16(b);
+    r7 = b;
+#pragma unroll
+    for (int d = 8; d < kFastLevels; ++d) {
+        const uint32_t c = col[d];
+        const uint32_t nc = and3(orand(c, pmr, a), rotr1(a), rotl1(b));
+        a = c;
+        col[d] = nc;
+        b = nc;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t mk = ((1u << (31 - 2 * k)) - 1u) << k;  // bits [k, 30-k]
+        w[k] = (col[k] & mk) | (col[15 - k] & ~mk);
+    }
+}
+
+// Band tier DC over columns 1..n of a window (m, n >= 1), every column in its
+// virtual band [o_j, o_j + 31]; band bits below absolute bit 0 are virtual
+// rows, active (0) like the zeros sh() shifts in: the mismatch word is masked
+// to real bits.  In band coordinates R[d][j] bit x depends on R[d][j-1] bit x
+// and R[d-1] bits x-1 (column j), x and x+1 (column j-1), so the bits a
+// traceback of a d_min <= 15 window can read -- level e's bits [e, 30-e] --
+// depend only on the same ranges one level down: every other bit may hold
+// anything.  Hence the D/I shifts are plain rotations (what wraps lands on bit
+// 0 or 31, outside every level >= 1's range), and levels 8..15 run rotated by
+// 16 -- the position their bits take in the paired words -- so pairing is one
+// LOP3 per word.  col[] ends as R[d][n]; tab.put(j, w) receives each column's
+// 8 paired words from column jstore on: the traceback of a window with
+// d_min <= 15 never reads a column below n - budget - 15 (it consumes at most
+// budget-1 pattern and d_min deletion steps before its last step).  Returns
+// the mask of levels d <= 15 with R[d][n] bit m-1 (band bit 15) active.
 template <class Tab>
 GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, int jstore, Tab& tab) {
     uint32_t col[kFastLevels];
     const int o0 = m - n - 16;
 #pragma unroll
-    for (int d = 0; d < kFastLevels; ++d) col[d] = init_band(m, d, o0);
+    for (int d = 0; d < kFastLevels; ++d) {
+        const uint32_t v = init_band(m, d, o0);
+        col[d] = d < 8 ? v : rot16(v);
+    }
+    uint32_t r7 = rot16(col[7]);
     uint32_t w[8];
     // columns with o_j <= 0: the band reaches below bit 0
     int jA = -o0;
@@ -255,46 +323,20 @@ GA_HD uint32_t dc_band(const Planes& pp, const Planes& tp, int m, int n, int jst
         const uint32_t valid = sh < 32 ? ~0u << sh : 0u;
         const uint32_t pm = pm_word((uint32_t)(pp.b0 << sh), (uint32_t)(pp.b1 << sh),
                                     (uint32_t)(pp.bn << sh), tp, j - 1) & valid;
-        uint32_t a = col[0];
-        uint32_t b = a | pm;
-        col[0] = b;
-#pragma unroll
-        for (int d = 1; d < kFastLevels; ++d) {
-            const uint32_t c = col[d];
-            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), shl1_or(b, 0u));
-            a = c;
-            col[d] = nc;
-            b = nc;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
+        band_column(col, r7, pm, w);
         if (j >= jstore) tab.put(j, w);
     }
-    // columns with o_j >= 1; four operations per entry
 #pragma unroll 1
     for (int j = jA + 1; j <= n; ++j) {
         const int oj = o0 + j;
         const uint32_t pm = pm_word((uint32_t)(pp.b0 >> oj), (uint32_t)(pp.b1 >> oj),
                                     (uint32_t)(pp.bn >> oj), tp, j - 1);
-        uint32_t a = col[0];
-        uint32_t b = a | pm;
-        col[0] = b;
-#pragma unroll
-        for (int d = 1; d < kFastLevels; ++d) {
-            const uint32_t c = col[d];
-            const uint32_t nc = and3(orand(c, pm, a), shr1_fill(a), shl1_or(b, 1u));
-            a = c;
-            col[d] = nc;
-            b = nc;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = pair_word(col[k], col[15 - k], k);
+        band_column(col, r7, pm, w);
         if (j >= jstore) tab.put(j, w);
     }
-    // success bit m-1 sits at band bit m-1-o_n = 15
     uint32_t ok = 0;
 #pragma unroll
-    for (int d = 0; d < kFastLevels; ++d) ok |= ((~col[d] >> 15) & 1u) << d;
+    for (int d = 0; d < kFastLevels; ++d) ok |= ((~col[d] >> (d < 8 ? 15 : 31)) & 1u) << d;
     return ok;
 }
 

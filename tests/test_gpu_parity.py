@@ -72,8 +72,8 @@ def test_align_errors_and_types(gpu):
     with pytest.raises(AttributeError):
         r.cost = 7
     assert gpu.align_batch([], gpu.WindowConfig()) == []
-    with pytest.raises(ValueError):
-        gpu.align("ACGT", "ACGT", gpu.WindowConfig(mode="baseline"))
+    rb = gpu.align("ACGT", "AGGT", gpu.WindowConfig(mode="baseline"))  # the unimproved engine
+    assert (rb.cigar, rb.cost, rb.rows_computed) == ("=X==", 1, 65)
 
 
 def test_fuzz_vs_reference_golden(gpu):

@@ -18,7 +18,13 @@ from paper_2203_15561_b200 import _abi, sim  # noqa: E402
 from oracle import oracle  # noqa: E402
 import corpus  # noqa: E402
 
-M = C.CDLL(os.path.join(ROOT, "tools", "_thread_model.so"))
+_SO = os.path.join(ROOT, "tools", "_thread_model.so")
+_SRC = [os.path.join(ROOT, "tools", "thread_model.cpp"),
+        os.path.join(ROOT, "paper_2203_15561_b200", "csrc", "genasm_thread.cuh")]
+if not os.path.exists(_SO) or any(os.path.getmtime(f) > os.path.getmtime(_SO) for f in _SRC):
+    import subprocess
+    subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", _SO, _SRC[0]], check=True)
+M = C.CDLL(_SO)
 
 
 def model(batch, w, o, k, prio):
