@@ -570,6 +570,17 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
 #ifdef GA_THREAD_STATS
         GA_STAT(5, clock64() - th0);
 #endif
+#ifndef GA_NO_DISCARD
+        // the step's tables are dead once every lane has traced back: drop
+        // their L2 lines without write-back, so they neither go to DRAM nor
+        // crowd out the tables other warps are still reading
+        __syncwarp();
+#pragma unroll 4
+        for (int l = lane; l < kBandWordsPerWarp * 4 / 128; l += 32)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(region) + l * 128)
+                         : "memory");
+        __syncwarp();
+#endif
     }
 
 #ifdef GA_THREAD_STATS
