@@ -29,7 +29,7 @@ namespace genasm {
 #ifdef GA_THREAD_STATS
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
-__device__ unsigned long long g_thread_stats[8];
+__device__ unsigned long long g_thread_stats[10];  // [8] band DC cycles, [9] band TB cycles
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
 #define GA_STAT(k, v) ((void)0)
@@ -194,7 +194,15 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
         ok = true;
     } else {
         const Planes tp = load_planes_bits(P.planes, P.plane_words, L.txt + L.t, w.n);
+#ifdef GA_THREAD_STATS
+        const int lane = threadIdx.x & 31;
+        const long long c0 = clock64();
+#endif
         uint32_t okm = dc_band(pp, tp, w.m, w.n, band_jstore(w.n, w.budget), bt);
+#ifdef GA_THREAD_STATS
+        const long long c1 = clock64();
+        GA_STAT(8, c1 - c0);
+#endif
         const int lim = K < 15 ? K : 15;
         okm &= (2u << lim) - 1u;
         if (!okm) {
@@ -206,6 +214,9 @@ __device__ __forceinline__ int band_window(const KernelParams& P, Lane& L, BandT
         }
         d_min = __ffs(okm) - 1;
         ok = tb_band<false>(bt, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, L.nops, o);
+#ifdef GA_THREAD_STATS
+        GA_STAT(9, clock64() - c1);
+#endif
     }
     if (!ok) {
         finish(P, L, 3);
@@ -698,9 +709,9 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
 
 #ifdef GA_THREAD_STATS
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 8);
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 10);
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, ~0ull, 0};
+        unsigned long long z[10] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
     }
 }
