@@ -29,7 +29,7 @@ namespace genasm {
 #ifdef GA_THREAD_STATS
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
-__device__ unsigned long long g_thread_stats[10];  // [8] band DC cycles, [9] band TB cycles
+__device__ unsigned long long g_thread_stats[12];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
 #define GA_STAT(k, v) ((void)0)
@@ -440,7 +440,13 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
     if (w.n == 0) {  // R[d][0] = init(m, d) solves iff d >= m
         d_min = w.m <= P.k ? w.m : -1;
     } else {
+#ifdef GA_THREAD_STATS
+        const long long c0 = clock64();
+#endif
         d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, pmt, lane);
+#ifdef GA_THREAD_STATS
+        GA_STAT(10, clock64() - c0);
+#endif
         if (d_min < 0 && P.k > kmax) return true;
     }
     if (d_min < 0) {
@@ -450,8 +456,14 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
         int64_t nops = (int64_t)shfl64((uint64_t)L.nops, owner);
         uint8_t* ops = P.ops + (int64_t)shfl64((uint64_t)L.ops, owner);
         thr::TbOut o;
+#ifdef GA_THREAD_STATS
+        const long long c1 = clock64();
+#endif
         const bool ok = coop_tb(ftab, pp, tp, w.m, w.n, d_min, w.budget, P.prio_lut, ops, nops, o,
                                 lane);
+#ifdef GA_THREAD_STATS
+        GA_STAT(11, clock64() - c1);
+#endif
         if (lane == owner) {
             L.nops = nops;
             if (ok) book(P, L, w, d_min, o);
@@ -709,9 +721,9 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
 
 #ifdef GA_THREAD_STATS
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 10);
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 12);
     if (reset) {
-        unsigned long long z[10] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0};
+        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
     }
 }
