@@ -405,9 +405,42 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     for (int64_t q = 1; q < n && chunks > 1; ++q)
         if (out->ops_off[q] < out->ops_off[q - 1] || out->win_off[q] < out->win_off[q - 1])
             chunks = 1;
+    // chunk boundaries: equal by default; GA_CHUNK_PLAN="w0,w1,..." weights (a
+    // small first chunk starts the kernels early, a small last one shortens
+    // the drain)
+    std::vector<int64_t> cut;
+    {
+        std::vector<double> wts;
+        const char* plan = getenv("GA_CHUNK_PLAN");
+        for (const char* s = plan; s && *s;) {
+            char* end = nullptr;
+            const double v = strtod(s, &end);
+            if (end == s) break;
+            if (v > 0) wts.push_back(v);
+            s = *end == ',' ? end + 1 : end;
+        }
+        if (!plan && chunks == 4 && n >= 72000) {
+            // measured on config 3 (tools/e2e_sweep.py): byte input is copy-bound
+            // and likes more, shorter-edged chunks; 2-bit input is kernel-bound
+            if (in->packed2) wts = {1, 2, 2, 1};
+            else wts = {1, 3, 3, 3, 3, 1};
+        }
+        if (wts.size() < 2 || (int64_t)wts.size() > n) wts.assign((size_t)chunks, 1.0);
+        if (chunks == 1) wts.assign(1, 1.0);
+        chunks = (int)wts.size();
+        double tot = 0, acc = 0;
+        for (double v : wts) tot += v;
+        cut.push_back(0);
+        for (double v : wts) {
+            acc += v;
+            cut.push_back(std::min<int64_t>(n, (int64_t)(n * (acc / tot) + 0.5)));
+        }
+        cut.back() = n;
+    }
     int64_t launches = 0;
     for (int k = 0; k < chunks; ++k) {
-        const int64_t q0 = n * k / chunks, q1 = n * (k + 1) / chunks;
+        const int64_t q0 = cut[k], q1 = cut[k + 1];
+        if (q1 <= q0) continue;
         const int64_t m = q1 - q0;
         Slot& S = c->slot[k % kSlots];
         // the symbol range the chunk reads

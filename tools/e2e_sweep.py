@@ -48,8 +48,13 @@ def main():
     }
     bout = _abi.GaBatchOut(h_res.data_ptr(), h[5].data_ptr(), h_ops.data_ptr(), out.n_ops,
                            h[6].data_ptr(), h_dst.data_ptr(), int(h_dst.shape[0]), 1)
-    for chunks in os.environ.get("SWEEP", "1,2,3,4,6,8").split(","):
-        os.environ["GA_CHUNKS"] = chunks
+    plans = os.environ.get("SWEEP_PLAN")
+    settings = plans.split(";") if plans else os.environ.get("SWEEP", "1,2,3,4,6,8").split(",")
+    for chunks in settings:
+        if plans:
+            os.environ["GA_CHUNK_PLAN"] = chunks
+        else:
+            os.environ["GA_CHUNKS"] = chunks
         row = [f"chunks={chunks:>2}"]
         for name, bin_ in bins.items():
             ts = []
