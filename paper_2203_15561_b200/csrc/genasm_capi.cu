@@ -96,7 +96,7 @@ struct Slot {
     }
 };
 
-constexpr int kSlots = 6;
+constexpr int kSlots = 8;
 
 struct ga_ctx {
     int device = 0;
@@ -420,9 +420,9 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
             s = *end == ',' ? end + 1 : end;
         }
         if (!plan && chunks == 4 && n >= 72000) {
-            // measured on config 3 (tools/e2e_sweep.py): six chunks, one slot
-            // each, the first and last small
-            wts = {1, 3, 3, 3, 3, 1};
+            // measured on config 3 (tools/e2e_sweep.py): eight chunks, one slot
+            // each, the first and last half-size
+            wts = {1, 2, 2, 2, 2, 2, 2, 1};
         }
         if (wts.size() < 2 || (int64_t)wts.size() > n) wts.assign((size_t)chunks, 1.0);
         if (chunks == 1) wts.assign(1, 1.0);
