@@ -104,29 +104,38 @@ uint64_t derive(uint64_t seed, uint64_t salt) { return seed * kMul + salt + kInc
 
 // simulate_read (sim.py:68-103); writes codes when out != null; returns length
 int64_t sim_one(const uint8_t* ref, int64_t pos, int32_t length, double sub, double ins,
-                double dele, uint64_t seed, uint8_t* out) {
+                double dele, uint64_t seed, uint8_t* out, char* ops = nullptr,
+                int64_t* n_ops = nullptr) {
     MT rng;
     rng.seed_u64(derive(derive(seed, (uint64_t)pos), (uint64_t)length));
     const double sub_edge = dele + sub;
-    int64_t n = 0;
+    int64_t n = 0, k = 0;  // read symbols, truth ops
     for (int64_t x = pos; x < pos + length; ++x) {
         const uint8_t base = ref[x];
         if (rng.random() < ins) {
             uint8_t c = (uint8_t)rng.randbelow(4);
             if (out) out[n] = c;
-            n++;
+            if (ops) ops[k] = 'I';
+            n++, k++;
         }
         const double draw = rng.random();
-        if (draw < dele) continue;
+        if (draw < dele) {
+            if (ops) ops[k] = 'D';
+            k++;
+            continue;
+        }
         if (draw < sub_edge) {
             uint8_t r = (uint8_t)rng.randbelow(3);  // "ACGT".replace(base, "")[r]
             uint8_t c = r < base ? r : (uint8_t)(r + 1);
             if (out) out[n] = c;
+            if (ops) ops[k] = 'X';
         } else {
             if (out) out[n] = base;
+            if (ops) ops[k] = '=';
         }
-        n++;
+        n++, k++;
     }
+    if (n_ops) *n_ops = k;
     return n;
 }
 
@@ -167,6 +176,14 @@ void ga_sim_reference(int64_t length, uint64_t seed, uint8_t* out) {
 int64_t ga_sim_read(const uint8_t* ref, int64_t pos, int32_t length, double sub, double ins,
                     double dele, uint64_t seed, uint8_t* out) {
     return sim_one(ref, pos, length, sub, ins, dele, seed, out);
+}
+
+// simulate_read with its ground truth (sim.py:68-103, SimRecord): the read's
+// codes and the edit script in reference order ('I', 'D', 'X', '='; up to
+// 2 * length ops); returns the read length, *n_ops the script length
+int64_t ga_sim_read_truth(const uint8_t* ref, int64_t pos, int32_t length, double sub, double ins,
+                          double dele, uint64_t seed, uint8_t* out, char* ops, int64_t* n_ops) {
+    return sim_one(ref, pos, length, sub, ins, dele, seed, out, ops, n_ops);
 }
 
 // CLI recipe positions (cli.py:141-144): read i has length read_lens[i]

@@ -34,6 +34,10 @@ def _lib():
         L.ga_sim_read.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_double,
                                   C.c_double, C.c_uint64, C.c_void_p]
         L.ga_sim_read.restype = C.c_int64
+        L.ga_sim_read_truth.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_double,
+                                        C.c_double, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.POINTER(C.c_int64)]
+        L.ga_sim_read_truth.restype = C.c_int64
         L.ga_sim_positions.argtypes = [C.c_int64, C.c_int64, C.c_void_p, C.c_uint64, C.c_void_p]
         L.ga_sim_positions.restype = None
         L.ga_sim_read_lengths.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
@@ -78,6 +82,22 @@ def simulate_read(ref: np.ndarray, pos: int, length: int, sub: float, ins: float
     out = np.empty(2 * length, dtype=np.uint8)
     n = _lib().ga_sim_read(ref.ctypes.data, pos, length, sub, ins, dele, seed, out.ctypes.data)
     return out[:n].copy()
+
+
+def simulate_read_truth(ref: np.ndarray, pos: int, length: int, sub: float, ins: float,
+                        dele: float, seed: int) -> tuple[np.ndarray, str]:
+    """``simulate_read(...)`` (sim.py:68-103) as (read codes, edit script): the
+    script's run-length form is ``SimRecord.truth_cigar`` and its non-'=' count
+    ``truth_cost``."""
+    ref = np.ascontiguousarray(ref, dtype=np.uint8)
+    if pos < 0 or length < 1 or pos + length > ref.shape[0]:
+        raise ValueError("slice out of range")
+    out = np.empty(2 * length, dtype=np.uint8)
+    ops = C.create_string_buffer(2 * length)
+    k = C.c_int64(0)
+    n = _lib().ga_sim_read_truth(ref.ctypes.data, pos, length, sub, ins, dele, seed,
+                                 out.ctypes.data, ops, C.byref(k))
+    return out[:n].copy(), ops.raw[:k.value].decode("ascii")
 
 
 def recipe_pairs(ref: np.ndarray, count: int, read_lens, sub: float, ins: float, dele: float,

@@ -13,6 +13,7 @@ Output (committed): tests/golden/cli.json with
     parse   [text, parse_cigar result or "CigarError: ..."]
     fasta   name -> [text, read_fasta records or error, write_fasta(records, width 7)]
     dp      [pattern, text, global_distance, semiglobal_distance or null]
+    simulate  [{argv, code, err, files: suffix -> content}]  `simulate` runs
 """
 
 from __future__ import annotations
@@ -105,6 +106,20 @@ BENCH_RUNS = [
 ]
 
 
+SIM_RUNS = [
+    ["--ref-len", "2000", "--count", "5", "--read-len", "300", "--seed", "11", "--emit-pairs"],
+    ["--ref-len", "100", "--count", "0", "--read-len", "50", "--seed", "1"],
+    ["--ref-len", "5000", "--count", "40", "--read-len", "97", "--sub", "0.1", "--ins", "0.2",
+     "--del", "0.3", "--seed", "77", "--emit-pairs"],
+    ["--ref-len", "30000", "--count", "12", "--read-len", "2500", "--sub", "0.01", "--ins", "0.07",
+     "--del", "0.07", "--seed", "10003"],
+    ["--ref-len", "100", "--count", "1", "--read-len", "50", "--sub", "0.9", "--ins", "0.2"],
+    ["--ref-len", "10", "--count", "1", "--read-len", "50"],
+    ["--ref-len", "0", "--count", "1", "--read-len", "5"],
+    ["--ref-len", "100", "--count", "1", "--read-len", "50", "--del", "-0.5"],
+]
+
+
 def _run(path: str, argv: list[str], cmd: str = "align") -> dict:
     out, err = io.StringIO(), io.StringIO()
     with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
@@ -157,6 +172,20 @@ def main() -> None:
                                   buf.getvalue()]
         except rio.MalformedFasta as exc:
             res["fasta"][name] = [text, f"MalformedFasta: {exc}", None]
+    res["simulate"] = []
+    for argv in SIM_RUNS:
+        with tempfile.TemporaryDirectory() as tmp:
+            prefix = os.path.join(tmp, "s")
+            out, err = io.StringIO(), io.StringIO()
+            with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+                code = rcli.main(["simulate", *argv, "--out-prefix", prefix])
+            files = {}
+            for suffix in ("ref.fasta", "reads.fasta", "truth.tsv", "pairs.tsv"):
+                if os.path.exists(f"{prefix}_{suffix}"):
+                    with open(f"{prefix}_{suffix}", encoding="utf-8") as fh:
+                        files[suffix] = fh.read()
+            res["simulate"].append({"argv": argv, "code": code, "err": err.getvalue(),
+                                    "files": files})
     rng = random.Random(99)
     res["dp"] = []
     for q in range(120):

@@ -179,3 +179,19 @@ def test_format_align_rows(ops2):
         assert text_m.decode("utf-8") == "".join(exp_m)
         checked += 1
     assert checked >= 10
+
+
+@pytest.mark.parametrize("run", GOLD["simulate"], ids=[" ".join(r["argv"]) for r in GOLD["simulate"]])
+def test_simulate_matches_reference(run, tmp_path, capsys):
+    """`simulate` (host code over the bit-exact simulator port): the four files,
+    stderr and exit code equal to the reference CLI's."""
+    from paper_2203_15561_b200 import cli
+    prefix = str(tmp_path / "s")
+    code = cli.main(["simulate", *run["argv"], "--out-prefix", prefix])
+    err = capsys.readouterr().err
+    files = {}
+    for suffix in ("ref.fasta", "reads.fasta", "truth.tsv", "pairs.tsv"):
+        path = f"{prefix}_{suffix}"
+        if os.path.exists(path):
+            files[suffix] = open(path, encoding="utf-8").read()
+    assert (code, err, files) == (run["code"], run["err"], run["files"])
