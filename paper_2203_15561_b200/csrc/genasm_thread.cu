@@ -20,7 +20,9 @@
 // Tables, per warp, in the context's scratch slab.  Band tier:
 // [column][word quad][lane] x 16 B -- each column's 16 levels are 8 paired
 // words (genasm_thread.cuh), two coalesced 16-byte stores per lane.  Full
-// tier (one window at a time, the same region): [column][level] x 8 B.
+// tier (one window at a time, the same region): [pass][wavefront step][level]
+// x 8 B (full_index).  At the end of each step the warp discards its region's
+// L2 lines: the tables are dead and need no write-back.
 #include "genasm_device.cuh"
 #include "genasm_thread.cuh"
 
@@ -663,7 +665,8 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const char* cap_env = getenv("GA_WARPS_PER_SM");
-    // 12 warps per SM measured best on config 3 (11-14 within 1 %)
+    // 16 warps per SM measured best on config 3 (12: 3 % slower; 20 at a
+    // 96-register cap: 13 % slower)
     const int warps_cap = cap_env && atoi(cap_env) > 0 ? atoi(cap_env) : 16;
     const int bcap = warps_cap / kWarps;
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
