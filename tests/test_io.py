@@ -195,3 +195,22 @@ def test_simulate_matches_reference(run, tmp_path, capsys):
         if os.path.exists(path):
             files[suffix] = open(path, encoding="utf-8").read()
     assert (code, err, files) == (run["code"], run["err"], run["files"])
+
+
+def test_groundtruth_symbol_ids():
+    """The DP kernel's inputs: per-character ids in the batch layout, ACGT at
+    0..3, every other character its own id (so 'N' matches 'N', 'N' != 'X')."""
+    from paper_2203_15561_b200.groundtruth import _symbol_batch
+    pairs = [("ACGTN", "NXAC"), ("é#", ""), ("", "TT")]
+    b = _symbol_batch(pairs)
+    assert b.pat_len.tolist() == [5, 2, 0] and b.txt_len.tolist() == [4, 0, 2]
+    seq = "".join(p + t for p, t in pairs)
+    ids = b.codes[:len(seq)].tolist()
+    assert ids[:4] == [0, 1, 2, 3]
+    for x, cx in zip(seq, ids):
+        for y, cy in zip(seq, ids):
+            assert (x == y) == (cx == cy)
+    lp = fmt.parse_pairs_bytes(b"a\tACGTN\tNXac\n", symbols=True)
+    assert lp.syms[:9].tolist()[:4] == [0, 1, 2, 3]
+    s = lp.syms[:9].tolist()
+    assert s[4] == s[5] and s[5] != s[6] and s[7:9] == [0, 1]  # N == N, N != X, 'ac' -> A, C
