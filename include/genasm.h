@@ -153,7 +153,8 @@ int ga_edit_distance(ga_ctx* ctx, const ga_batch_in* in, int32_t semiglobal, int
 
 /* Same call over DEVICE-resident buffers (every pointer in `in` and `out`
  * is a device pointer on the context's device).  Asynchronous on
- * `stream` (a cudaStream_t; NULL = the context's own stream). */
+ * `stream` (a cudaStream_t; NULL = the context's own stream).  1-byte codes
+ * in, ASCII ops out: packed2 / ops2 return -3. */
 int ga_align_batch_device(ga_ctx* ctx, const ga_batch_in* in, const ga_config* cfg,
                           ga_batch_out* out, void* stream);
 

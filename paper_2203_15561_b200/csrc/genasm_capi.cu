@@ -367,6 +367,11 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
         return -2;
     }
     c->launches = 0;
+    if (in->packed2 || out->ops2) {  // the transfer formats belong to the host-buffer call
+        c->err = "ga_align_batch_device takes 1-byte codes and writes ASCII ops (packed2/ops2 are "
+                 "ga_align_batch formats)";
+        return -3;
+    }
     if (in->n_pairs <= 0) return 0;
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");

@@ -305,6 +305,10 @@ def test_device_call_vs_oracle(gpu, oracle_mod):
                              dists=dst.cpu().numpy(), n_ops=host.n_ops)
     exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
     _packed_equal(got, exp, "device call")
+    # the 2-bit transfer formats belong to the host-buffer call
+    din.packed2 = 1
+    assert L.ga_align_batch_device(ctx, C.byref(din), C.byref(cfg), C.byref(dout), None) == -3
+    assert b"packed2" in L.ga_last_error(ctx)
 
 
 def test_baseline_mode_vs_oracle(gpu, oracle_mod):
