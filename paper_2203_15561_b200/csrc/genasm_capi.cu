@@ -398,6 +398,18 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
                 return -3;
             }
     }
+    // every sequence inside codes_len, every pair's outputs inside the capacities
+    for (int64_t q = 0; q < n; ++q) {
+        const int64_t lp = in->pat_len[q], lt = in->txt_len[q];
+        if (lp < 0 || lt < 0 || in->pat_off[q] < 0 || in->txt_off[q] < 0 ||
+            in->pat_off[q] + lp > in->codes_len || in->txt_off[q] + lt > in->codes_len ||
+            out->ops_off[q] < 0 || out->ops_off[q] + lp + lt > out->ops_capacity ||
+            out->win_off[q] < 0 ||
+            out->win_off[q] + ga_num_windows(lp, cfg->window, cfg->overlap) > out->win_capacity) {
+            c->err = "pair " + std::to_string(q) + ": a sequence or output range is out of bounds";
+            return -3;
+        }
+    }
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
 
