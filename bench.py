@@ -330,6 +330,14 @@ def main():
     e2e_pk_value = pairs_all * args.e2e_steps / e2e_pk_s
     if not np.array_equal(res_bytes, h_res.numpy()):
         raise RuntimeError("packed-input and byte-input host runs disagree")
+    # variant: byte codes in, the call packs each chunk on the host (GA_PACK_HOST)
+    hin_hp = _abi.GaBatchIn(n, h_in[0].data_ptr(), int(batch.codes.shape[0]), h_in[1].data_ptr(),
+                            h_in[2].data_ptr(), h_in[3].data_ptr(), h_in[4].data_ptr(), None,
+                            _abi.GA_PACK_HOST)
+    e2e_hp_s = e2e_run(hin_hp, args.e2e_steps)
+    e2e_hp_value = pairs_all * args.e2e_steps / e2e_hp_s
+    if not np.array_equal(res_bytes, h_res.numpy()):
+        raise RuntimeError("packed-input and byte-input host runs disagree")
     h2d_pk = h2d - int(h_in[0].shape[0]) + int(h_pk.shape[0]) + 8 * int(packed.exceptions.shape[0])
 
     # device path and host path must agree exactly
@@ -413,7 +421,12 @@ def main():
                             "results + distances + 2-bit ops out, chunked copy/kernel overlap",
                     "packed_input": {"value": e2e_pk_value, "h2d_bytes_per_step": h2d_pk,
                                      "path": "same call with ga_batch_in.packed2 (sequences "
-                                             "held 2 bits/symbol on the host; packing not timed)"}},
+                                             "held 2 bits/symbol on the host; packing not timed)"},
+                    "host_pack": {"value": e2e_hp_value,
+                                  "h2d_bytes_per_step": h2d_pk - 8 * int(packed.exceptions.shape[0]),
+                                  "path": "same call on the same byte input with ga_batch_in.packed2 "
+                                          "= GA_PACK_HOST (each chunk packed to 2 bits on the host "
+                                          "inside the call, timed)"}},
             "gpu_launches": launches, "clocks": clock_info,
             "extra": {"hbm": hbm, "status_counts": status_counts, "windows": work.windows,
                       "dc_entries": work.entries, "tb_steps": work.tb_steps,

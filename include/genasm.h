@@ -49,12 +49,15 @@ typedef struct {
 
 enum { GA_MODE_IMPROVED = 0, GA_MODE_BASELINE = 1 };
 
+/* ga_batch_in.packed2 */
+enum { GA_PACK_NONE = 0, GA_PACK_CALLER = 1, GA_PACK_HOST = 2 };
+
 /* A batch of (pattern, text) pairs: the `pairs` list of align_batch.
  * All sequences live in one code array; offsets index into it. */
 typedef struct {
     int64_t        n_pairs;
     const uint8_t* codes;      /* symbol codes 0..4 (one byte per symbol), or 2-bit
-                                  packed ACGT when packed2 != 0 */
+                                  packed ACGT when packed2 == GA_PACK_CALLER */
     int64_t        codes_len;  /* symbols in `codes`; must cover every offset + length
                                   (the device call converts exactly this range) */
     const int64_t* pat_off;    /* offsets and lengths are in symbols */
@@ -65,9 +68,16 @@ typedef struct {
                                   0..n_pairs-1, longest first for load balance);
                                   NULL: ga_align_batch computes it on the host,
                                   ga_align_batch_device uses input order */
-    /* ga_align_batch only: 2-bit input, four symbols per byte (symbol x in
-     * bits 2(x%4)..2(x%4)+1 of byte x/4, 0..3 = ACGT); the positions of
-     * symbols outside ACGT (code 4) are listed in `exceptions` (ascending). */
+    /* ga_align_batch only, the input transfer format:
+     * 0 (GA_PACK_NONE): `codes` are 1-byte codes, copied as they are;
+     * 1 (GA_PACK_CALLER): 2-bit input, four symbols per byte (symbol x in
+     *   bits 2(x%4)..2(x%4)+1 of byte x/4, 0..3 = ACGT); the positions of
+     *   symbols outside ACGT (code 4) are listed in `exceptions` (ascending);
+     * 2 (GA_PACK_HOST): `codes` are 1-byte codes; the call packs each
+     *   pipeline chunk to 2 bits on the host (ga_pack2, into pinned staging)
+     *   while the previous chunk's copy is in flight, and copies that --
+     *   a quarter of the PCIe bytes.  n_exceptions/exceptions are ignored.
+     * Other values return -3. */
     int32_t        packed2;
     int64_t        n_exceptions;
     const int64_t* exceptions;

@@ -36,6 +36,10 @@ class GaBatchIn(C.Structure):
                 ("exceptions", C.c_void_p)]
 
 
+# ga_batch_in.packed2 (include/genasm.h)
+GA_PACK_NONE, GA_PACK_CALLER, GA_PACK_HOST = 0, 1, 2
+
+
 class GaBatchOut(C.Structure):
     _fields_ = [("results", C.c_void_p), ("ops_off", C.c_void_p), ("ops", C.c_void_p),
                 ("ops_capacity", C.c_int64), ("win_off", C.c_void_p),
@@ -142,7 +146,7 @@ class PackedBatch:
                       None if order is None else order.ctypes.data)
         if packed is not None:
             s.codes = packed.data.ctypes.data
-            s.packed2 = 1
+            s.packed2 = GA_PACK_CALLER
             s.n_exceptions = int(packed.exceptions.shape[0])
             s.exceptions = packed.exceptions.ctypes.data if packed.exceptions.shape[0] else None
         return s

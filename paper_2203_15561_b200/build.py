@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "_genasm.so")
 SOURCES = ["genasm_lockstep.cu", "genasm_thread.cu", "genasm_capi.cu", "genasm_pack.cu", "sim.cpp",
-           "accounting.cpp", "microbench.cu", "genasm_io.cpp", "genasm_baseline.cu", "genasm_dp.cu"]
+           "accounting.cpp", "microbench.cu", "genasm_io.cpp", "genasm_baseline.cu", "genasm_dp.cu", "pack_host.cpp"]
 HEADERS = ["genasm_kernel.cuh", "genasm_device.cuh", "genasm_thread.cuh", "../../include/genasm.h",
            "../../include/genasm_sim.h", "../../include/genasm_bench.h", "../../include/genasm_io.h"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -50,6 +50,25 @@ struct DevBuf {
     }
 };
 
+struct HostBuf {  // pinned host staging
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && ptr) return cudaSuccess;
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        cap = 0;
+        cudaError_t e = cudaHostAlloc(&ptr, bytes, cudaHostAllocDefault);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
 // Scratch one kernel launch owns: the work queue head and the overflow slabs
 // + band tables.  Chunks in flight on different slots use different scratch,
 // so their kernels can overlap (the next chunk fills SMs as one drains).
@@ -79,6 +98,7 @@ struct Scratch {
 //   int64 pat_off[m] | txt_off[m] | ops_off[m] | win_off[m] | int32 pat_len[m] | txt_len[m] | order[m]
 struct Slot {
     DevBuf codes, packed, exc, meta, results, ops, ops2, dists;
+    HostBuf h_pack, h_exc;  // packed2 == GA_PACK_HOST: this chunk's 2-bit symbols
     void* h_meta = nullptr;
     size_t h_meta_cap = 0;
     Scratch scratch;
@@ -87,6 +107,8 @@ struct Slot {
     bool used = false;  // in_done/out_done have been recorded
     void release() {
         for (DevBuf* b : {&codes, &packed, &exc, &meta, &results, &ops, &ops2, &dists}) b->release();
+        h_pack.release();
+        h_exc.release();
         if (h_meta) cudaFreeHost(h_meta);
         h_meta = nullptr;
         scratch.release();
@@ -390,7 +412,14 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
     }
     const int64_t n = in->n_pairs;
     c->launches = 0;
+    if (in->packed2 < 0 || in->packed2 > GA_PACK_HOST) {
+        c->err = "packed2 must be 0 (bytes), 1 (2-bit input) or 2 (bytes packed per chunk by the call)";
+        return -3;
+    }
     if (n <= 0) return 0;
+    // 2-bit transfer: the caller's packed array (1) or per-chunk packing into
+    // pinned staging here, overlapping the previous chunk's copy (2)
+    const bool xfer2 = in->packed2 != 0, host_pack = in->packed2 == GA_PACK_HOST;
     if (out->ops2) {
         for (int64_t q = 0; q < n; ++q)
             if (out->ops_off[q] & 3) {
@@ -479,12 +508,12 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
             ohi = q1 < n ? out->ops_off[q1] : out->ops_capacity;
             whi = q1 < n ? out->win_off[q1] : out->win_capacity;
         }
-        const int64_t base = in->packed2 ? (lo & ~int64_t(3)) : lo;
+        const int64_t base = xfer2 ? (lo & ~int64_t(3)) : lo;
         const int64_t nsym = hi - base;
         const int64_t nops = ohi - olo;
         const int64_t nwin = whi - wlo;
         int64_t nexc = 0, exc0 = 0;
-        if (in->packed2 && in->n_exceptions > 0) {
+        if (in->packed2 == 1 && in->n_exceptions > 0) {
             const int64_t* x0 = std::lower_bound(in->exceptions, in->exceptions + in->n_exceptions, base);
             const int64_t* x1 = std::lower_bound(x0, in->exceptions + in->n_exceptions, hi);
             exc0 = x0 - in->exceptions;
@@ -519,8 +548,19 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
             (e = S.results.ensure((size_t)m * sizeof(ga_pair_result))) ||
             (e = S.ops.ensure((size_t)nops + 16)) || (e = S.dists.ensure((size_t)nwin + 16)))
             return fail(c, e, "cudaMalloc");
-        if (in->packed2 && ((e = S.packed.ensure((size_t)(nsym + 3) / 4 + 16)) ||
-                            (e = S.exc.ensure((size_t)(nexc > 0 ? nexc : 1) * 8))))
+        if (host_pack) {  // pack [base, hi) into the slot's pinned staging (free: in_done passed)
+            const size_t pk = (size_t)(nsym + 3) / 4 + 16;
+            if ((e = S.h_pack.ensure(pk)) || (e = S.h_exc.ensure(S.h_exc.cap ? S.h_exc.cap : 8192)))
+                return fail(c, e, "cudaHostAlloc");
+            nexc = ga_pack2(in->codes + base, nsym, (uint8_t*)S.h_pack.ptr, (int64_t*)S.h_exc.ptr,
+                            (int64_t)(S.h_exc.cap / 8));
+            if ((size_t)nexc * 8 > S.h_exc.cap) {  // rare: more code-4 symbols than staged room
+                if ((e = S.h_exc.ensure((size_t)nexc * 8))) return fail(c, e, "cudaHostAlloc");
+                ga_pack2(in->codes + base, nsym, (uint8_t*)S.h_pack.ptr, (int64_t*)S.h_exc.ptr, nexc);
+            }
+        }
+        if (xfer2 && ((e = S.packed.ensure((size_t)(nsym + 3) / 4 + 16)) ||
+                      (e = S.exc.ensure((size_t)(nexc > 0 ? nexc : 1) * 8))))
             return fail(c, e, "cudaMalloc");
         if (out->ops2 && (e = S.ops2.ensure((size_t)(nops + 3) / 4 + 16)))
             return fail(c, e, "cudaMalloc");
@@ -533,7 +573,10 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
         };
         e = h2d(S.meta.ptr, S.h_meta, meta_bytes);
         if (!e) {
-            if (in->packed2) {
+            if (host_pack) {
+                e = h2d(S.packed.ptr, S.h_pack.ptr, (size_t)(nsym + 3) / 4);
+                if (!e && nexc) e = h2d(S.exc.ptr, S.h_exc.ptr, (size_t)nexc * 8);
+            } else if (xfer2) {
                 e = h2d(S.packed.ptr, in->codes + base / 4, (size_t)(nsym + 3) / 4);
                 if (!e && nexc) e = h2d(S.exc.ptr, in->exceptions + exc0, (size_t)nexc * 8);
             } else {
@@ -546,11 +589,11 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
 
         // ---- the slot's kernel stream: expand 2-bit sequences, align, pack ops ----
         if ((e = cudaStreamWaitEvent(sk, S.in_done, 0))) return fail(c, e, "wait");
-        if (in->packed2) {
+        if (xfer2) {  // host-packed exceptions are chunk-relative already
             if ((e = genasm::launch_unpack2((const uint8_t*)S.packed.ptr, nsym, (uint8_t*)S.codes.ptr,
                                             sk)) ||
-                (e = genasm::launch_patch((const int64_t*)S.exc.ptr, nexc, base, (uint8_t*)S.codes.ptr,
-                                          sk)))
+                (e = genasm::launch_patch((const int64_t*)S.exc.ptr, nexc, host_pack ? 0 : base,
+                                          (uint8_t*)S.codes.ptr, sk)))
                 return fail(c, e, "unpack kernel");
             launches += 1 + (nexc > 0);
         }

@@ -97,6 +97,11 @@ cudaError_t launch_pack_ops(const uint8_t* ascii, int64_t nops, uint8_t* out, cu
 
 }  // namespace genasm
 
+namespace genasm {
+bool host_has_avx2();                                              // pack_host.cpp
+int64_t pack2_avx2(const uint8_t* codes, int64_t nblk, uint8_t* out);  // pack_host.cpp
+}  // namespace genasm
+
 extern "C" {
 
 // 8 code bytes -> 2 packed bytes (low 2 bits of each code, symbol order kept)
@@ -116,10 +121,16 @@ int64_t ga_pack2(const uint8_t* codes, int64_t n, uint8_t* packed, int64_t* exce
     // per-thread ranges of 64 symbols (16 packed bytes)
     const int64_t chunk = ((nbytes + nth - 1) / nth + 15) / 16 * 16;
     std::vector<int64_t> counts((size_t)nth, 0);
+    static const bool avx2 = genasm::host_has_avx2();
     auto work = [&](int w) {
         const int64_t b0 = std::min(nbytes, w * chunk), b1 = std::min(nbytes, b0 + chunk);
         int64_t cnt = 0;
         int64_t b = b0;
+        if (avx2) {  // 32 symbols per iteration
+            const int64_t nblk = std::max<int64_t>(0, std::min(b1 - b0, n / 4 - b0) / 8);
+            cnt += genasm::pack2_avx2(codes + 4 * b0, nblk, packed + b0);
+            b += 8 * nblk;
+        }
         for (; b + 2 <= b1 && 4 * b + 8 <= n; b += 2) {  // 8 symbols per iteration
             uint64_t v;
             memcpy(&v, codes + 4 * b, 8);

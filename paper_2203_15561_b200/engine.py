@@ -125,10 +125,13 @@ def pack2(codes: np.ndarray) -> _abi.Packed2:
 
 def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: str,
                device: int | None = None, *, packed2: bool = False,
-               ops2: bool = False, mode: str = "improved") -> PackedResults:
+               ops2: bool = False, mode: str = "improved",
+               host_pack: bool = False) -> PackedResults:
     """One ga_align_batch call on one device (host buffers in and out).
-    packed2 / ops2 select the 2-bit transfer formats of include/genasm.h;
-    mode="baseline" runs the unimproved engine (dense edge tables)."""
+    packed2 / ops2 select the 2-bit transfer formats of include/genasm.h
+    (packed2: packed here first, GA_PACK_CALLER); host_pack: the call packs
+    each pipeline chunk itself (GA_PACK_HOST); mode="baseline" runs the
+    unimproved engine (dense edge tables)."""
     dev = _default_device() if device is None else int(device)
     ctx = context(dev)
     out = PackedResults.allocate(batch, window, overlap, ops2=ops2)
@@ -137,6 +140,8 @@ def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: 
     cfg = _abi.make_config(window, overlap, k, priority, mode)
     packed = pack2(batch.codes) if packed2 else None  # must outlive the call
     bin_ = batch.struct(packed=packed)
+    if host_pack and not packed2:
+        bin_.packed2 = _abi.GA_PACK_HOST
     bout = out.struct()
     with _ctx_locks[dev]:
         rc = lib().ga_align_batch(ctx, C.byref(bin_), C.byref(cfg), C.byref(bout))

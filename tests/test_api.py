@@ -143,9 +143,10 @@ def test_capi_host_functions():
 def test_transfer_formats_host_side():
     """ga_pack2 (2-bit input + exception list) and the ops2 decoders."""
     rng = np.random.default_rng(3)
-    for n in (0, 1, 3, 4, 5, 1023, 100_003, 2_000_003):
+    for n in (0, 1, 3, 4, 5, 31, 32, 33, 1023, 100_003, 2_000_003, 3_000_064):
         codes = rng.integers(0, 4, n).astype(np.uint8)
         codes[rng.random(n) < 0.01] = 4
+        codes[n // 3:n // 3 + 70] = 4  # whole 32-symbol blocks of code 4 (vector path)
         p = engine.pack2(codes)
         assert p.data.shape[0] == max(1, (n + 3) // 4)
         unpacked = ((p.data[:, None] >> np.array([0, 2, 4, 6], np.uint8)) & 3).reshape(-1)[:n]

@@ -200,6 +200,34 @@ def test_transfer_formats(gpu, oracle_mod, packed2, ops2):
         assert got.cigar(q) == exp.ops[o:o + n].tobytes().decode(), q
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_host_pack(gpu, oracle_mod, monkeypatch, chunks):
+    """GA_PACK_HOST: byte codes (with code-4 symbols) packed per chunk by the
+    call itself give the oracle's results; bad packed2 values are refused."""
+    import ctypes as C
+    from paper_2203_15561_b200 import _abi, engine, sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(5, count=2000)
+    batch = _with_exceptions(batch)
+    monkeypatch.setenv("GA_CHUNKS", str(chunks))
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    for ops2 in (False, True):
+        got = run_packed(batch, 64, 24, 64, "MSID", host_pack=True, ops2=ops2)
+        assert np.array_equal(got.results, exp.results)
+        assert np.array_equal(got.dists, exp.dists)
+        for q in range(batch.n_pairs):
+            n = int(exp.results["ops_len"][q])
+            o = int(exp.ops_off[q])
+            assert got.cigar(q) == exp.ops[o:o + n].tobytes().decode(), q
+    out = _abi.PackedResults.allocate(batch, 64, 24)
+    bin_, bout = batch.struct(), out.struct()
+    bin_.packed2 = 3
+    cfg = _abi.make_config(64, 24, 64, "MSID")
+    L, ctx = engine.lib(), engine.context(0)
+    assert L.ga_align_batch(ctx, C.byref(bin_), C.byref(cfg), C.byref(bout)) == -3
+    assert b"packed2" in L.ga_last_error(ctx)
+
+
 @pytest.mark.parametrize("chunks", [1, 2, 3, 7])
 def test_chunked_pipeline(gpu, monkeypatch, chunks):
     """Chunked, stream-overlapped host path == one-shot path (ga_align_batch)."""
@@ -209,8 +237,8 @@ def test_chunked_pipeline(gpu, monkeypatch, chunks):
     monkeypatch.setenv("GA_CHUNKS", "1")
     ref = run_packed(batch, 64, 24, 64, "MSID")
     monkeypatch.setenv("GA_CHUNKS", str(chunks))
-    for packed2, ops2 in [(False, False), (True, True)]:
-        got = run_packed(batch, 64, 24, 64, "MSID", packed2=packed2, ops2=ops2)
+    for packed2, ops2, hp in [(False, False, False), (True, True, False), (False, True, True)]:
+        got = run_packed(batch, 64, 24, 64, "MSID", packed2=packed2, ops2=ops2, host_pack=hp)
         assert np.array_equal(got.results, ref.results)
         assert np.array_equal(got.dists, ref.dists)
         for q in range(0, batch.n_pairs, 7):
