@@ -69,6 +69,9 @@ def main():
               f"warps finish own pairs over {(st[7] - st[6]) / 1e6:.2f} ms; lane 0 band DC cycles/step "
               f"{st[8] / max(st[0], 1):.0f} band TB cycles/step {st[9] / max(st[0], 1):.0f}; full-tier DC "
               f"cycles/window {st[10] / max(st[2], 1):.0f} TB {st[11] / max(st[2], 1):.0f}")
+    import hashlib
+    dig = hashlib.md5(res.cpu().numpy().tobytes() + dst.cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"results+dists md5 {dig}")
     print(f"config {cfg_id} n={n} ms/launch {[round(x, 2) for x in times]} "
           f"best {min(times):.2f} ({n / min(times) * 1e3 / 1e6:.3f} M aln/s) "
           f"status {np.bincount(r['status'], minlength=4).tolist()}", flush=True)
