@@ -443,7 +443,10 @@ GA_HD uint64_t diag_eq(const Planes& pp, const Planes& tp, int s) {
     return ~((a0 ^ tp.b0) | (a1 ^ tp.b1) | an | tp.bn);
 }
 
-constexpr int kRun = 8;  // '=' steps speculated per round trip
+#ifndef GA_KRUN
+#define GA_KRUN 8
+#endif
+constexpr int kRun = GA_KRUN;  // '=' steps speculated per round trip
 
 // Traceback of one window (backtrace.py:88-160), from (j=n, d=d_min, i=m-1)
 // until the budget is consumed.  BIT(e, c, x) returns table bit x of level e,
