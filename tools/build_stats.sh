@@ -4,4 +4,4 @@
 cd "$(dirname "$0")/../paper_2203_15561_b200/csrc" && \
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -DGA_THREAD_STATS \
   -Xcompiler -fPIC,-O3,-pthread -shared -cudart static -o ../../tools/_genasm_stats.so \
-  genasm_lockstep.cu genasm_thread.cu genasm_capi.cu genasm_pack.cu sim.cpp accounting.cpp microbench.cu genasm_io.cpp genasm_baseline.cu genasm_dp.cu
+  genasm_lockstep.cu genasm_thread.cu genasm_capi.cu genasm_pack.cu sim.cpp accounting.cpp microbench.cu genasm_io.cpp genasm_baseline.cu genasm_dp.cu pack_host.cpp
