@@ -67,7 +67,11 @@ typedef struct {
     const int32_t* order;      /* optional processing order (a permutation of
                                   0..n_pairs-1, longest first for load balance);
                                   NULL: ga_align_batch computes it on the host,
-                                  ga_align_batch_device uses input order */
+                                  ga_align_batch_device uses input order.
+                                  ga_align_batch checks it is a permutation (-3
+                                  otherwise) and uses it only when the batch runs
+                                  as one chunk: a chunked batch orders each chunk
+                                  longest-first itself */
     /* ga_align_batch only, the input transfer format:
      * 0 (GA_PACK_NONE): `codes` are 1-byte codes, copied as they are;
      * 1 (GA_PACK_CALLER): 2-bit input, four symbols per byte (symbol x in

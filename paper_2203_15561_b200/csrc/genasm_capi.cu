@@ -403,6 +403,8 @@ int ga_align_batch_device(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg
     return rc;
 }
 
+static int align_chunks(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out);
+
 int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out) {
     if (!c) return -1;
     char msg[160];
@@ -417,9 +419,6 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
         return -3;
     }
     if (n <= 0) return 0;
-    // 2-bit transfer: the caller's packed array (1) or per-chunk packing into
-    // pinned staging here, overlapping the previous chunk's copy (2)
-    const bool xfer2 = in->packed2 != 0, host_pack = in->packed2 == GA_PACK_HOST;
     if (out->ops2) {
         for (int64_t q = 0; q < n; ++q)
             if (out->ops_off[q] & 3) {
@@ -439,9 +438,39 @@ int ga_align_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_ba
             return -3;
         }
     }
+    if (in->order) {  // a caller's order must be a permutation of 0..n-1
+        std::vector<uint8_t> seen((size_t)n, 0);
+        for (int64_t q = 0; q < n; ++q) {
+            const int32_t v = in->order[q];
+            if (v < 0 || v >= n || seen[(size_t)v]) {
+                c->err = "order is not a permutation of 0.." + std::to_string(n - 1) +
+                         " (entry " + std::to_string(q) + ")";
+                return -3;
+            }
+            seen[(size_t)v] = 1;
+        }
+    }
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(c, e, "cudaSetDevice");
+    const int rc = align_chunks(c, in, cfg, out);
+    if (rc != 0) {
+        // chunks already enqueued may still be copying into the caller's
+        // buffers: drain every stream before the error reaches the caller
+        cudaStreamSynchronize(c->stream_in);
+        for (Slot& sl : c->slot)
+            if (sl.stream) cudaStreamSynchronize(sl.stream);
+        cudaStreamSynchronize(c->stream_out);
+    }
+    return rc;
+}
 
+// the chunked pipeline of ga_align_batch (inputs validated by the caller)
+static int align_chunks(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, ga_batch_out* out) {
+    const int64_t n = in->n_pairs;
+    // 2-bit transfer: the caller's packed array (1) or per-chunk packing into
+    // pinned staging here, overlapping the previous chunk's copy (2)
+    const bool xfer2 = in->packed2 != 0, host_pack = in->packed2 == GA_PACK_HOST;
+    cudaError_t e;
     // ---- chunk plan: consecutive pairs, pipelined over kSlots slots.  Chunking
     // needs output offsets that grow with the input index (the prefix-sum
     // layout every caller in this package uses); otherwise one chunk. ----

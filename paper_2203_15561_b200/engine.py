@@ -170,8 +170,13 @@ def _subset(batch: PackedBatch, idx: np.ndarray) -> PackedBatch:
                        txt_off=batch.txt_off[idx], txt_len=batch.txt_len[idx])
 
 
-def _scatter(full: PackedResults, part: PackedResults, idx: np.ndarray, batch: PackedBatch) -> None:
+def _scatter(full: PackedResults, part: PackedResults, idx: np.ndarray, batch: PackedBatch,
+             window: int, overlap: int) -> None:
+    """Copy one shard's records, ops and window distances to their input
+    positions in `full` (the reference returns slots in input order,
+    window.py:152-163)."""
     full.results[idx] = part.results
+    n_win = _abi.num_windows(batch.pat_len[idx], window, overlap)
     for local, q in enumerate(idx.tolist()):
         n_ops = int(part.results["ops_len"][local])
         src = int(part.ops_off[local])
@@ -181,9 +186,11 @@ def _scatter(full: PackedResults, part: PackedResults, idx: np.ndarray, batch: P
             full.ops[dst // 4:dst // 4 + nb] = part.ops[src // 4:src // 4 + nb]
         else:
             full.ops[dst:dst + n_ops] = part.ops[src:src + n_ops]
+        # the pair's own window count (App. A.4), not the distance to the next
+        # offset: allocate() pads an all-empty shard's distance array to 1
         w_src = int(part.win_off[local])
         w_dst = int(full.win_off[q])
-        w_n = (int(part.win_off[local + 1]) if local + 1 < len(idx) else part.dists.shape[0]) - w_src
+        w_n = int(n_win[local])
         full.dists[w_dst:w_dst + w_n] = part.dists[w_src:w_src + w_n]
 
 
@@ -218,5 +225,5 @@ def run_batch(batch: PackedBatch, cfg, devices=None) -> PackedResults:
     full = PackedResults.allocate(batch, cfg.window, cfg.overlap)
     for s, idx in enumerate(shards):
         if len(idx):
-            _scatter(full, parts[s], idx, batch)
+            _scatter(full, parts[s], idx, batch, cfg.window, cfg.overlap)
     return full
