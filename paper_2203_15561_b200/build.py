@@ -2,7 +2,9 @@
 
 Produces paper_2203_15561_b200/_genasm.so: the fused DC+TB kernel, the C-ABI
 host side and the workload generator, cudart linked statically so the .so
-loads on the GPU box without a toolkit path.
+loads on the GPU box without a toolkit path.  check=True builds the same
+library with the kernel's contract checks (-DGA_CHECK, the PrunedAccess /
+bounds tripwires) into _genasm_check.so, for tests/test_check_build.py.
 """
 
 from __future__ import annotations
@@ -14,6 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "_genasm.so")
+CHECK_SO = os.path.join(HERE, "_genasm_check.so")
 SOURCES = ["genasm_lockstep.cu", "genasm_thread.cu", "genasm_capi.cu", "genasm_pack.cu", "sim.cpp",
            "accounting.cpp", "microbench.cu", "genasm_io.cpp", "genasm_baseline.cu", "genasm_dp.cu", "pack_host.cpp"]
 HEADERS = ["genasm_kernel.cuh", "genasm_device.cuh", "genasm_thread.cuh", "../../include/genasm.h",
@@ -29,28 +32,29 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def needs_build() -> bool:
-    if not os.path.exists(SO):
+def needs_build(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return SO
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
+    so = CHECK_SO if check else SO
+    if not force and not needs_build(so):
+        return so
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", SO + ".tmp", *srcs]
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DGA_CHECK"] if check else []), "-o", so + ".tmp", *srcs]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc failed building _genasm.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(so)}")
     if verbose:
         sys.stderr.write(proc.stderr)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, check="--check" in sys.argv)

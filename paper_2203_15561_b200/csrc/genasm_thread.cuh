@@ -557,22 +557,27 @@ GA_HD int band_jstore(int n, int budget) {
 }
 
 // Traceback of a band-tier window: the walk of traceback() with the level
-// bits read from the band table (tab.wi(e): the word of level e, tab.bit(w, e,
-// b): its bit at band position b, relative to each column's virtual band
-// origin o_j) and the '=' test from the symbol planes.
-
+// bits read from a band table.  Tab supplies the table format:
+//   Tab::Word          the stored word type (32-bit band tier, 64-bit wide tier)
+//   Tab::kHalf         band half-width: column j keeps absolute pattern bits
+//                      [o_j, o_j + 2 kHalf), o_j = m - n + j - kHalf
+//   tab.get(e, c)      the word of column c >= 1 that holds level e
+//   tab.bit(w, e, x)   level e's bit at band position x of such a word
+// and the '=' test comes from the symbol planes.
+//
 // kWriteEq = false: the ops buffer was pre-filled with '=', only the other ops
 // are written
-template <bool kWriteEq = true, class Tab>
+template <bool kWriteEq = true, int kR = kRun, class Tab>
 GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
                    int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
+    using Word = typename Tab::Word;
     constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
     int d = d_min, j = n, i = m - 1;
-    const int o0 = m - n - 16;
+    const int o0 = m - n - Tab::kHalf;
     o.consumed = o.tcons = o.wcost = 0;
     o.reads = 0;
     // with '=' first in priority a step is '=' iff its match edge is active:
-    // runs of them along a diagonal are found kRun at a time, their table
+    // runs of them along a diagonal are found kR at a time, their table
     // words loaded together
     const bool m_first = ((prio_lut >> 60) & 0xFu) == OPC_M;  // all four edges active -> M
     int s_eq = 1 << 30;
@@ -592,30 +597,28 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             int K = j - 1;
             K = K < i ? K : i;
             K = K < budget - o.consumed ? K : budget - o.consumed;
-            K = K < kRun ? K : kRun;
+            K = K < kR ? K : kR;
             const int sd = i - (j - 1);  // diagonal: pattern index - text index
             if (sd != s_eq) {
                 s_eq = sd;
                 eqv = diag_eq(pp, tp, sd);
             }
             const int u = i - (o0 + j);
-            const int kd = tab.wi(d);
             const int dm1 = d > 0 ? d - 1 : 0;
-            const int ke = tab.wi(dm1);
             // level d and d-1 words of columns j-1-k; level d-1 of column j too: the
             // step that ends the run reads from them as well
-            uint32_t w[kRun], v[kRun];
+            Word w[kR], v[kR];
 #pragma unroll
-            for (int k = 0; k < kRun; ++k) {
-                w[k] = k < K ? tab.get(kd, j - 1 - k) : 0u;
-                v[k] = k < K ? tab.get(ke, j - 1 - k) : 0u;
+            for (int k = 0; k < kR; ++k) {
+                w[k] = k < K ? tab.get(d, j - 1 - k) : Word(0);
+                v[k] = k < K ? tab.get(dm1, j - 1 - k) : Word(0);
             }
-            const uint32_t vj = tab.get(ke, j);
+            const Word vj = tab.get(dm1, j);
             // step k sits at (i-k, j-k): '=' iff symbols match and R[d][j-1-k] bit i-1-k
             // (band position u) is active
             unsigned okm = 0;
 #pragma unroll
-            for (int k = 0; k < kRun; ++k) {
+            for (int k = 0; k < kR; ++k) {
                 const uint32_t eq = (uint32_t)(eqv >> ((j - 1 - k) & 63)) & 1u;
                 okm |= (eq & ~tab.bit(w[k], d, u)) << k;
             }
@@ -632,9 +635,9 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
             if (run == K) continue;  // limits reached: re-check at the new state
             // the step at (i, j) = run end: its '=' edge is inactive; the others
             // come from the words already loaded (j >= 2, i >= 1 here)
-            uint32_t wr = v[0], wp = vj;
+            Word wr = v[0], wp = vj;
 #pragma unroll
-            for (int k = 1; k < kRun; ++k) {
+            for (int k = 1; k < kR; ++k) {
                 wr = run == k ? v[k] : wr;
                 wp = run == k ? v[k - 1] : wp;
             }
@@ -660,11 +663,11 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
         if (j == 0) continue;
         const int u = i - (o0 + j);  // band position of (i, j); (i-1, j-1) shares it
         const int dm1 = d > 0 ? d - 1 : 0;
-        const uint32_t wj = tab.get(tab.wi(dm1), j);
+        const Word wj = tab.get(dm1, j);
         uint32_t mb, sb, db;
         if (j >= 2) {
-            const uint32_t w1 = tab.get(tab.wi(d), j - 1);
-            const uint32_t w2 = tab.get(tab.wi(dm1), j - 1);
+            const Word w1 = tab.get(d, j - 1);
+            const Word w2 = tab.get(dm1, j - 1);
             mb = tab.bit(w1, d, u);
             sb = tab.bit(w2, dm1, u);
             db = tab.bit(w2, dm1, u + 1);
@@ -700,6 +703,168 @@ GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, i
         o.tcons += mj;
         o.wcost += md;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Wide tier (16 <= d_min <= 31): the band of the band tier widened to the 64
+// diagonals delta in [-32, 31] (column j keeps bits [O_j, O_j + 63],
+// O_j = m - n + j - 32; band bit X <-> delta = 31 - X, success at X = 31).
+// The band tier's argument with 32 for 16: a cell the traceback of a window
+// with d_min <= 31 reads at level e has |delta| <= 31 - e, i.e. X in
+// [e, 62 - e], and those bits depend only on the same ranges one level down,
+// so the 64-bit D/I shifts are rotations as well.  Levels 0..16 are computed
+// 64 bits wide (8 instructions per entry), levels 17..31 (|delta| <= 14) in
+// the 32-bit sub-band X in [16, 47], rotated by 16 like the band tier's upper
+// levels (4 instructions per entry); level 16 feeds them through one LOP3.
+//
+// Paired storage, the band tier's trick at 64 bits: level e <= 15 needs
+// X in [e, 62 - e] (63 - 2e bits), level 31 - e needs X in [31 - e, 31 + e]
+// (2e + 1 bits) -- rotated by 32 (the two 32-bit halves swapped) exactly the
+// bits level e leaves free.  The rotated-by-16 32-bit form of level 31 - e
+// has those bits at the same positions in both halves, so pair k (levels k
+// and 31 - k) is two LOP3s: 16 pairs, 32 words (128 B) per column.
+// ---------------------------------------------------------------------------
+constexpr int kWideLevels = 32;
+
+// low word of (hi:lo) >> 1 and of (hi:lo) << 1 >> 32
+GA_HD uint32_t fsr1(uint32_t lo, uint32_t hi) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(lo, hi, 1);
+#else
+    return (lo >> 1) | (hi << 31);
+#endif
+}
+GA_HD uint32_t fsl1(uint32_t lo, uint32_t hi) {  // (hi << 1) | (lo >> 31)
+#ifdef __CUDA_ARCH__
+    return __funnelshift_l(lo, hi, 1);
+#else
+    return (hi << 1) | (lo >> 31);
+#endif
+}
+// the 32-bit sub-band X in [16, 47] of a 64-bit band row, rotated by 16
+GA_HD uint32_t sub16(uint32_t lo, uint32_t hi) {
+    return (lo & 0xffff0000u) | (hi & 0x0000ffffu);  // one LOP3
+}
+
+GA_HD uint64_t init_band64(int m, int d, int org) {
+    const int z = (d < m ? d : m) - org;  // zero below band bit z
+    if (z <= 0) return ~0ull;
+    if (z >= 64) return 0ull;
+    return ~((1ull << z) - 1ull);
+}
+
+GA_HD uint64_t shl64(uint64_t x, int s) { return s < 64 ? x << s : 0ull; }
+
+// one wide-tier column: cl/ch = levels 0..16 (64-bit), r = levels 17..31
+// (sub-band, rotated), r16 = level 16 of the previous column (sub-band,
+// rotated); when `store`, tab.put4(j, q, w) receives the column's 32 paired
+// words four at a time (so only four are live at once)
+template <class Tab>
+GA_HD void wide_column(uint32_t* cl, uint32_t* ch, uint32_t* r, uint32_t& r16, uint32_t pml,
+                       uint32_t pmh, bool store, int j, Tab& tab) {
+    uint32_t al = cl[0], ah = ch[0];
+    uint32_t bl = al | pml, bh = ah | pmh;  // level 0: the match edge only
+    cl[0] = bl;
+    ch[0] = bh;
+#pragma unroll
+    for (int d = 1; d <= 16; ++d) {
+        const uint32_t c_l = cl[d], c_h = ch[d];
+        // D: (a >> 1), I: (b << 1), both as 64-bit rotations
+        const uint32_t nl = and3(orand(c_l, pml, al), fsr1(al, ah), fsl1(bh, bl));
+        const uint32_t nh = and3(orand(c_h, pmh, ah), fsr1(ah, al), fsl1(bl, bh));
+        al = c_l;
+        ah = c_h;
+        cl[d] = nl;
+        ch[d] = nh;
+        bl = nl;
+        bh = nh;
+    }
+    uint32_t b = sub16(bl, bh);
+    uint32_t a = r16;
+    r16 = b;
+    const uint32_t pmr = sub16(pml, pmh);
+#pragma unroll
+    for (int d = 17; d < kWideLevels; ++d) {
+        const uint32_t c = r[d - 17];
+        const uint32_t nc = and3(orand(c, pmr, a), rotr1(a), rotl1(b));
+        a = c;
+        r[d - 17] = nc;
+        b = nc;
+    }
+    if (!store) return;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = 2 * q + h;
+            const uint32_t s = k == 15 ? r16 : r[14 - k];  // level 31 - k
+            const uint32_t mlo = 0xffffffffu << k;        // X in [k, 31]
+            const uint32_t mhi = 0xffffffffu >> (k + 1);  // X in [32, 62 - k]
+            w[2 * h] = (cl[k] & mlo) | (s & ~mlo);
+            w[2 * h + 1] = (ch[k] & mhi) | (s & ~mhi);
+        }
+        tab.put4(j, q, w);
+    }
+}
+
+// Wide tier DC over columns 1..n (m, n >= 1); tab.put4 receives each
+// column's 32 paired words from column jstore on.  Returns the mask of levels
+// d <= 31 with R[d][n] bit m-1 (band bit 31) active.
+template <class Tab>
+GA_HD uint32_t dc_wide(const Planes& pp, const Planes& tp, int m, int n, int jstore, Tab& tab) {
+    uint32_t cl[17], ch[17], r[15];
+    const int O0 = m - n - 32;
+#pragma unroll
+    for (int d = 0; d <= 16; ++d) {
+        const uint64_t v = init_band64(m, d, O0);
+        cl[d] = (uint32_t)v;
+        ch[d] = (uint32_t)(v >> 32);
+    }
+    uint32_t r16 = sub16(cl[16], ch[16]);
+#pragma unroll
+    for (int d = 17; d < kWideLevels; ++d) r[d - 17] = rot16(init_band(m, d, O0 + 16));
+#pragma unroll 1
+    for (int j = 1; j <= n; ++j) {
+        const int oj = O0 + j;
+        uint64_t a0, a1, an, valid;
+        if (oj < 0) {  // virtual bits below absolute bit 0: active, mismatch 0
+            a0 = shl64(pp.b0, -oj);
+            a1 = shl64(pp.b1, -oj);
+            an = shl64(pp.bn, -oj);
+            valid = shl64(~0ull, -oj);
+        } else {
+            a0 = pp.b0 >> oj;
+            a1 = pp.b1 >> oj;
+            an = pp.bn >> oj;
+            valid = ~0ull;
+        }
+        const uint32_t s0 = bcast(tp.b0, j - 1), s1 = bcast(tp.b1, j - 1), sn = bcast(tp.bn, j - 1);
+        const uint32_t pml = (((uint32_t)a0 ^ s0) | ((uint32_t)a1 ^ s1) | (uint32_t)an | sn) &
+                             (uint32_t)valid;
+        const uint32_t pmh = (((uint32_t)(a0 >> 32) ^ s0) | ((uint32_t)(a1 >> 32) ^ s1) |
+                              (uint32_t)(an >> 32) | sn) & (uint32_t)(valid >> 32);
+        wide_column(cl, ch, r, r16, pml, pmh, j >= jstore, j, tab);
+    }
+    uint32_t ok = 0;
+#pragma unroll
+    for (int d = 0; d <= 16; ++d) ok |= ((~cl[d] >> 31) & 1u) << d;
+#pragma unroll
+    for (int d = 17; d < kWideLevels; ++d) ok |= ((~r[d - 17] >> 31) & 1u) << d;
+    return ok;
+}
+
+// first table column the wide-tier traceback can read (see band_jstore)
+GA_HD int wide_jstore(int n, int budget) {
+    const int j = n - budget - 31;
+    return j > 1 ? j : 1;
+}
+
+// level e's pair in the wide table, and its bit at band position x of a pair
+// word (levels >= 16 are stored with the halves swapped)
+GA_HD int wide_pair(int e) { return e <= 15 ? e : 31 - e; }
+GA_HD uint32_t wide_bit(uint64_t w, int e, int x) {
+    return (uint32_t)(w >> ((e <= 15 ? x : x ^ 32) & 63)) & 1u;
 }
 
 // entry_writes of one window in closed form (dptable.py:62-82, 156-171):

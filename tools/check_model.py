@@ -50,7 +50,7 @@ def compare(batch, w, o, k, prio, tag):
         a, b = int(exp.win_off[q]), _abi.num_windows(int(batch.pat_len[q]), w, o)
         if not np.array_equal(got.dists[a:a + b], exp.dists[a:a + b]):
             bad.append(q)
-    print(f"{tag}: n={batch.n_pairs} tiers(band,full,n0)={tiers[:3].tolist()} bad={len(bad)}"
+    print(f"{tag}: n={batch.n_pairs} tiers(band,full,n0,wide)={tiers[:4].tolist()} bad={len(bad)}"
           + (f" first={bad[:3]} got={got.results[bad[0]]} exp={exp.results[bad[0]]}" if bad else ""),
           flush=True)
     return not bad

@@ -3,6 +3,7 @@
 // full-tier math can be checked against the oracle without a GPU.
 //   g++ -O2 -std=c++17 -shared -fPIC -o tools/_thread_model.so tools/thread_model.cpp
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -13,12 +14,26 @@
 using namespace genasm::thr;
 
 struct HostBand {
+    using Word = uint32_t;
+    static constexpr int kHalf = 16;
     std::vector<uint32_t> w;  // [column][8 paired words]
     void reset(int n) { w.assign((size_t)(n + 1) * 8, 0xdeadbeefu); }
     void put(int j, const uint32_t* pw) { memcpy(&w[(size_t)j * 8], pw, 32); }
-    uint32_t get(int k, int c) const { return w[(size_t)c * 8 + k]; }
-    int wi(int e) const { return packed_word(e); }
+    uint32_t get(int e, int c) const { return w[(size_t)c * 8 + packed_word(e)]; }
     uint32_t bit(uint32_t x, int e, int b) const { return packed_bit(x, e, b); }
+};
+
+struct HostWide {
+    using Word = uint64_t;
+    static constexpr int kHalf = 32;
+    std::vector<uint32_t> w;  // [column][32 paired words]
+    void reset(int n) { w.assign((size_t)(n + 1) * 32, 0xdeadbeefu); }
+    void put4(int j, int q, const uint32_t* pw) { memcpy(&w[(size_t)j * 32 + 4 * q], pw, 16); }
+    uint64_t get(int e, int c) const {
+        const size_t k = (size_t)c * 32 + 2 * wide_pair(e);
+        return (uint64_t)w[k + 1] << 32 | w[k];
+    }
+    uint32_t bit(uint64_t x, int e, int b) const { return wide_bit(x, e, b); }
 };
 
 struct HostFull {
@@ -40,7 +55,9 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
     if (W > 64) return -2;
     const uint64_t lut = make_prio_lut(cfg->priority);
     HostBand band;
+    HostWide wide;
     HostFull full;
+    const bool no_wide = getenv("MODEL_NO_WIDE") != nullptr;
     // the kernel's bit-plane form of the codes
     const int64_t pw = (in->codes_len + 63) / 64 + 1;
     std::vector<uint64_t> pl((size_t)pw * 3, 0);
@@ -101,6 +118,23 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                     status = GA_WINDOW_FAILED;
                     break;
                 } else {
+                    uint32_t wm = 0;
+                    if (!no_wide) {
+                        wide.reset(n);
+                        wm = dc_wide(pp, tp, m, n, wide_jstore(n, budget), wide);
+                        wm &= K < 31 ? (2u << K) - 1u : ~0u;
+                        if (wm & 0xffffu) return -10;  // the band tier is exact below 16
+                    }
+                    if (wm) {
+                        d_min = __builtin_ctz(wm);
+                        ok = tb_band(wide, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
+                        tier_counts[3]++;
+                        goto booked;
+                    }
+                    if (!no_wide && K <= 31) {
+                        status = GA_WINDOW_FAILED;
+                        break;
+                    }
                     full.reset((K + kPassLevels) / kPassLevels * kPassLevels, W);
                     d_min = dc_full(pp, tp, m, n, K, full);
                     if (d_min < 0) {
@@ -112,6 +146,7 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                     tier_counts[1]++;
                 }
             }
+        booked:
             if (!ok) {
                 status = GA_STUCK;
                 break;
