@@ -557,7 +557,154 @@ GA_HD int band_jstore(int n, int budget) {
 }
 
 // Traceback of a band-tier window: the walk of traceback() with the level
-// bits read from a band table.  Tab supplies the table format:
+// bits read from the band table (tab.wi(e): the word of level e, tab.bit(w, e,
+// b): its bit at band position b, relative to each column's virtual band
+// origin o_j) and the '=' test from the symbol planes.
+
+// kWriteEq = false: the ops buffer was pre-filled with '=', only the other ops
+// are written
+template <bool kWriteEq = true, class Tab>
+GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
+                   int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
+    constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
+    int d = d_min, j = n, i = m - 1;
+    const int o0 = m - n - 16;
+    o.consumed = o.tcons = o.wcost = 0;
+    o.reads = 0;
+    // with '=' first in priority a step is '=' iff its match edge is active:
+    // runs of them along a diagonal are found kRun at a time, their table
+    // words loaded together
+    const bool m_first = ((prio_lut >> 60) & 0xFu) == OPC_M;  // all four edges active -> M
+    int s_eq = 1 << 30;
+    uint64_t eqv = 0;
+    for (;;) {
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+            if (i + 1 > d) return false;
+            const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
+            for (int u = 0; u < take; ++u) ops[nops + u] = 'I';
+            nops += take;
+            o.wcost += take;
+            o.consumed += take;
+            return true;
+        }
+        if (m_first && j >= 2 && i >= 1) {
+            int K = j - 1;
+            K = K < i ? K : i;
+            K = K < budget - o.consumed ? K : budget - o.consumed;
+            K = K < kRun ? K : kRun;
+            const int sd = i - (j - 1);  // diagonal: pattern index - text index
+            if (sd != s_eq) {
+                s_eq = sd;
+                eqv = diag_eq(pp, tp, sd);
+            }
+            const int u = i - (o0 + j);
+            const int kd = tab.wi(d);
+            const int dm1 = d > 0 ? d - 1 : 0;
+            const int ke = tab.wi(dm1);
+            // level d and d-1 words of columns j-1-k; level d-1 of column j too: the
+            // step that ends the run reads from them as well
+            uint32_t w[kRun], v[kRun];
+#pragma unroll
+            for (int k = 0; k < kRun; ++k) {
+                w[k] = k < K ? tab.get(kd, j - 1 - k) : 0u;
+                v[k] = k < K ? tab.get(ke, j - 1 - k) : 0u;
+            }
+            const uint32_t vj = tab.get(ke, j);
+            // step k sits at (i-k, j-k): '=' iff symbols match and R[d][j-1-k] bit i-1-k
+            // (band position u) is active
+            unsigned okm = 0;
+#pragma unroll
+            for (int k = 0; k < kRun; ++k) {
+                const uint32_t eq = (uint32_t)(eqv >> ((j - 1 - k) & 63)) & 1u;
+                okm |= (eq & ~tab.bit(w[k], d, u)) << k;
+            }
+            okm &= (1u << K) - 1u;
+            const int run = (int)ctz32(~okm);
+            if (kWriteEq)
+                for (int k = 0; k < run; ++k) ops[nops + k] = '=';
+            nops += run;
+            j -= run;
+            i -= run;
+            o.consumed += run;
+            o.tcons += run;
+            o.reads += (int64_t)run * (d > 0 ? 3 : 1);
+            if (run == K) continue;  // limits reached: re-check at the new state
+            // the step at (i, j) = run end: its '=' edge is inactive; the others
+            // come from the words already loaded (j >= 2, i >= 1 here)
+            uint32_t wr = v[0], wp = vj;
+#pragma unroll
+            for (int k = 1; k < kRun; ++k) {
+                wr = run == k ? v[k] : wr;
+                wp = run == k ? v[k - 1] : wp;
+            }
+            const bool dpos = d > 0;
+            const bool sok = dpos && !tab.bit(wr, dm1, u);
+            const bool iok = dpos && !tab.bit(wp, dm1, u - 1);
+            const bool dok = dpos && !tab.bit(wr, dm1, u + 1);
+            const unsigned om = (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+            const int op = (int)((prio_lut >> (4 * om)) & 0xFu);
+            o.reads += dpos ? 3 : 1;
+            if (op > OPC_D) return false;
+            ops[nops++] = (uint8_t)(kChars >> (8 * op));
+            const int mj = op != OPC_I, mi = op != OPC_D;
+            j -= mj;
+            i -= mi;
+            d -= 1;
+            o.consumed += mi;
+            o.tcons += mj;
+            o.wcost += 1;
+            continue;
+        }
+        if (i < 0 || o.consumed >= budget) return true;
+        if (j == 0) continue;
+        const int u = i - (o0 + j);  // band position of (i, j); (i-1, j-1) shares it
+        const int dm1 = d > 0 ? d - 1 : 0;
+        const uint32_t wj = tab.get(tab.wi(dm1), j);
+        uint32_t mb, sb, db;
+        if (j >= 2) {
+            const uint32_t w1 = tab.get(tab.wi(d), j - 1);
+            const uint32_t w2 = tab.get(tab.wi(dm1), j - 1);
+            mb = tab.bit(w1, d, u);
+            sb = tab.bit(w2, dm1, u);
+            db = tab.bit(w2, dm1, u + 1);
+        } else {  // column 0 = init(m, .): bit x inactive iff x >= level
+            mb = i - 1 >= d;
+            sb = i - 1 >= d - 1;
+            db = i >= d - 1;
+        }
+        const uint32_t ib = tab.bit(wj, dm1, u - 1);
+        const bool symeq = !bit64(tp.bn, j - 1) && !bit64(pp.bn, i) &&
+                           bit64(tp.b0, j - 1) == bit64(pp.b0, i) &&
+                           bit64(tp.b1, j - 1) == bit64(pp.b1, i);
+        const bool dpos = d > 0;
+        const bool i0 = i == 0;
+        const bool mok = symeq && (i0 || !mb);
+        const bool sok = dpos && (i0 || !sb);
+        const bool iok = dpos && (i0 || !ib);
+        const bool dok = dpos && !db;
+        const unsigned okm =
+            (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+        const int op = (int)((prio_lut >> (4 * okm)) & 0xFu);
+        o.reads += (j >= 2) + (dpos ? (j >= 2) + 1 : 0);
+        if (op > OPC_D) return false;
+        if (kWriteEq || op != OPC_M) ops[nops] = (uint8_t)(kChars >> (8 * op));
+        ++nops;
+        const int mj = op != OPC_I;  // M, S, D consume a text symbol
+        const int mi = op != OPC_D;  // M, S, I consume a pattern symbol
+        const int md = op != OPC_M;
+        j -= mj;
+        i -= mi;
+        d -= md;
+        o.consumed += mi;
+        o.tcons += mj;
+        o.wcost += md;
+    }
+}
+
+// Traceback of a band window over any table format (the band tier's and the
+// wide tier's; tools/thread_model.cpp), the walk of traceback() with the level
+// bits read from the table.  Tab supplies the table format:
 //   Tab::Word          the stored word type (32-bit band tier, 64-bit wide tier)
 //   Tab::kHalf         band half-width: column j keeps absolute pattern bits
 //                      [o_j, o_j + 2 kHalf), o_j = m - n + j - kHalf
@@ -568,7 +715,7 @@ GA_HD int band_jstore(int n, int budget) {
 // kWriteEq = false: the ops buffer was pre-filled with '=', only the other ops
 // are written
 template <bool kWriteEq = true, int kR = kRun, class Tab>
-GA_HD bool tb_band(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
+GA_HD bool tb_band_t(Tab& tab, const Planes& pp, const Planes& tp, int m, int n, int d_min,
                    int budget, uint64_t prio_lut, uint8_t* ops, int64_t& nops, TbOut& o) {
     using Word = typename Tab::Word;
     constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;

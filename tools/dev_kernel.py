@@ -43,13 +43,13 @@ def main():
     dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
                            d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
     if hasattr(L, "ga_debug_thread_stats"):
-        z = np.zeros(20, np.uint64)
+        z = np.zeros(12, np.uint64)
         L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
     st = torch.cuda.Stream(dev)
     times = []
     for it in range(reps):
         if hasattr(L, "ga_debug_thread_stats") and it == reps - 1:
-            z = np.zeros(20, np.uint64)
+            z = np.zeros(12, np.uint64)
             L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -61,52 +61,15 @@ def main():
         times.append(a.elapsed_time(b))
     r = res.cpu().numpy().view(_abi.RESULT_DTYPE)
     if hasattr(L, "ga_debug_thread_stats"):
-        tl = np.zeros(512, np.uint64)
-        L.ga_debug_timeline(tl.ctypes.data_as(C.c_void_p))
-        steps, lanes = tl[:256].astype(np.float64), tl[256:].astype(np.float64)
-        last = int(np.nonzero(steps)[0].max()) + 1 if steps.any() else 0
-        print("timeline (ms: band steps k, lanes/step): " + " ".join(
-            f"{i}:{steps[i] / 1e3:.0f}k/{lanes[i] / max(steps[i], 1):.1f}" for i in range(last)))
-        if hasattr(L, "ga_debug_pair_times") and n <= 262144:
-            pt = np.zeros(3 * n, np.uint64)
-            L.ga_debug_pair_times(pt.ctypes.data_as(C.c_void_p), n)
-            t0 = pt[:n].min()
-            st_ms = (pt[:n] - t0) / 1e6
-            cta = (pt[2 * n:] & 0xffffffff).astype(np.int64)
-            ctasm = (pt[2 * n:] >> 32).astype(np.int64)
-            fin_ms = (pt[n:2 * n] - t0) / 1e6
-            np.savez_compressed(os.path.join("gpurun_out", f"pairtimes_cfg{cfg_id}.npz"), start=st_ms,
-                                fin=fin_ms, cta=cta, sm=ctasm, rows=res.cpu().numpy().view(_abi.RESULT_DTYPE)["rows_computed"])
-            import collections
-            by = collections.defaultdict(list)
-            for c, f in zip(cta.tolist(), fin_ms.tolist()):
-                by[c].append(f)
-            med = np.array([np.median(v) for v in by.values()])
-            spread = np.array([np.percentile(v, 90) - np.percentile(v, 10) for v in by.values() if len(v) > 5])
-            print(f"per-CTA median finish ms: min {med.min():.1f} p10 {np.percentile(med, 10):.1f} p50 "
-                  f"{np.median(med):.1f} p90 {np.percentile(med, 90):.1f} max {med.max():.1f}; within-CTA "
-                  f"p90-p10 spread median {np.median(spread):.1f} ms; pairs/CTA "
-                  f"{np.mean([len(v) for v in by.values()]):.0f}")
-            q = [0, 1, 10, 50, 90, 99, 99.9, 100]
-            print("pair start ms pct " + " ".join(f"{p}:{np.percentile(st_ms, p):.1f}" for p in q))
-            print("pair finish ms pct " + " ".join(f"{p}:{np.percentile(fin_ms, p):.1f}" for p in q))
-            dur = fin_ms - st_ms
-            print("pair duration ms pct " + " ".join(f"{p}:{np.percentile(dur, p):.1f}" for p in q))
-            hw = res.cpu().numpy().view(_abi.RESULT_DTYPE)
-            slow = np.argsort(-fin_ms)[:5]
-            print("slowest pairs (finish ms, rows_computed):", [(int(i), round(float(fin_ms[i]), 1), int(hw["rows_computed"][i])) for i in slow])
-        st = np.zeros(20, np.uint64)
+        st = np.zeros(12, np.uint64)
         L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
         st = st.astype(np.float64)  # the last launch only
         print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
-              f"hard steps {st[2]:.0f} hard windows {st[3]:.0f} ({st[3] / max(st[2], 1):.1f}/step) "
-              f"full-tier windows {st[10]:.0f}; cycles/band step {st[4] / max(st[0], 1):.0f} "
-              f"(DC {st[8] / max(st[0], 1):.0f} TB {st[9] / max(st[0], 1):.0f}) cycles/hard step "
-              f"{st[5] / max(st[2], 1):.0f} (full tier {st[11] / max(st[2], 1):.0f}); "
-              f"warp-time share hard {st[5] / max(st[4] + st[5], 1):.3f}; "
-              f"warps exit over {(st[7] - st[6]) / 1e6:.2f} ms; loop iterations {st[12]:.0f} claim cycles "
-              f"{st[13]:.3g} refill cycles {st[14]:.3g} idle cycles {st[15]:.3g} band {st[4]:.3g} "
-              f"hard {st[5]:.3g} loop {st[16] + st[17]:.3g} discard {st[18]:.3g} away lanes/step {st[19] / max(st[0], 1):.2f}")
+              f"full-tier windows {st[2]:.0f} hand-overs {st[3]:.0f} "
+              f"cycles/band step {st[4] / max(st[0], 1):.0f} full-tier cycles/step {st[5] / max(st[0], 1):.0f} "
+              f"warps finish own pairs over {(st[7] - st[6]) / 1e6:.2f} ms; lane 0 band DC cycles/step "
+              f"{st[8] / max(st[0], 1):.0f} band TB cycles/step {st[9] / max(st[0], 1):.0f}; full-tier DC "
+              f"cycles/window {st[10] / max(st[2], 1):.0f} TB {st[11] / max(st[2], 1):.0f}")
     import hashlib
     dig = hashlib.md5(res.cpu().numpy().tobytes() + dst.cpu().numpy().tobytes()).hexdigest()[:12]
     print(f"results+dists md5 {dig}")

@@ -112,7 +112,7 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                 okm &= (2u << lim) - 1u;
                 if (okm) {
                     d_min = __builtin_ctz(okm);
-                    ok = tb_band(band, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
+                    ok = tb_band_t(band, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
                     tier_counts[0]++;
                 } else if (K <= 15) {
                     status = GA_WINDOW_FAILED;
@@ -127,7 +127,7 @@ extern "C" int model_align_batch(const ga_batch_in* in, const ga_config* cfg, ga
                     }
                     if (wm) {
                         d_min = __builtin_ctz(wm);
-                        ok = tb_band(wide, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
+                        ok = tb_band_t(wide, pp, tp, m, n, d_min, budget, lut, ops, nops, o);
                         tier_counts[3]++;
                         goto booked;
                     }
