@@ -139,6 +139,10 @@ int ga_check_config(const ga_config* cfg, char* msg, int msg_len);
  * uppercase alphabet has masks). */
 void ga_encode_ascii(const char* seq, int64_t n, uint8_t* out);
 
+/* The same on `threads` host threads (0: all): the drop-in Python
+ * align_batch encodes its joined pair strings with it. */
+void ga_encode_ascii_mt(const char* seq, int64_t n, uint8_t* out, int32_t threads);
+
 /* Create a context bound to one CUDA device (one context per device; a
  * context is not re-entrant).  Returns 0 or a CUDA error code. */
 int ga_create(int device, ga_ctx** out);

@@ -355,3 +355,32 @@ int64_t ga_format_align_rows(int64_t n, const char* ids, const int64_t* id_off, 
 }
 
 }  // extern "C"
+
+extern "C" void ga_encode_ascii_mt(const char* seq, int64_t n, uint8_t* out, int32_t threads) {
+    // ACGT -> 0..3, everything else 4 (the reference's masks cover exactly the
+    // uppercase alphabet, pkg/src/bitalign/distance.py:70-79)
+    static const struct Lut {
+        uint8_t v[256];
+        Lut() {
+            memset(v, 4, sizeof v);
+            v[(unsigned char)'A'] = 0;
+            v[(unsigned char)'C'] = 1;
+            v[(unsigned char)'G'] = 2;
+            v[(unsigned char)'T'] = 3;
+        }
+    } lut;
+    int t = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+    if (t < 1) t = 1;
+    if (n < (int64_t)1 << 20) t = 1;
+    const int64_t per = (n + t - 1) / t;
+    auto work = [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) out[i] = lut.v[(unsigned char)seq[i]];
+    };
+    std::vector<std::thread> pool;
+    for (int k = 1; k < t; ++k) {
+        const int64_t a = k * per, b = std::min(n, a + per);
+        if (a < b) pool.emplace_back(work, a, b);
+    }
+    work(0, std::min(n, per));
+    for (auto& th : pool) th.join();
+}

@@ -50,6 +50,7 @@ def lib():
             "ga_num_windows": ([C.c_int64, C.c_int32, C.c_int32], C.c_int64),
             "ga_check_config": ([F, C.c_char_p, C.c_int], C.c_int),
             "ga_encode_ascii": ([C.c_char_p, C.c_int64, C.c_void_p], None),
+            "ga_encode_ascii_mt": ([C.c_char_p, C.c_int64, C.c_void_p, C.c_int32], None),
             "ga_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
             "ga_destroy": ([C.c_void_p], None),
             "ga_last_error": ([C.c_void_p], C.c_char_p),
@@ -149,6 +150,29 @@ def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: 
             raise RuntimeError(f"ga_align_batch failed ({rc}): "
                                f"{lib().ga_last_error(ctx).decode(errors='replace')}")
     return out
+
+
+def pack_pairs(pairs) -> PackedBatch:
+    """``PackedBatch.from_pairs`` for the drop-in ``align_batch``: the pair
+    strings joined once and encoded by the native multithreaded encoder
+    (ga_encode_ascii_mt) instead of a numpy table lookup; non-ASCII input
+    (Unicode code units, never a match) takes the exact Python path."""
+    import itertools
+    n = len(pairs)
+    lens = np.fromiter(map(len, itertools.chain.from_iterable(pairs)), dtype=np.int64,
+                       count=2 * n)
+    blob = "".join(itertools.chain.from_iterable(pairs))
+    if not blob.isascii():
+        return PackedBatch.from_pairs(pairs)
+    raw = blob.encode("ascii")
+    codes = np.empty(max(1, len(raw)), dtype=np.uint8)
+    lib().ga_encode_ascii_mt(raw, len(raw), codes.ctypes.data, 0)
+    starts = np.zeros(2 * n, dtype=np.int64)
+    if n:
+        np.cumsum(lens[:-1], out=starts[1:])
+    return PackedBatch(codes=codes[:len(raw)] if len(raw) else codes[:0],
+                       pat_off=starts[0::2].copy(), pat_len=lens[0::2].astype(np.int32),
+                       txt_off=starts[1::2].copy(), txt_len=lens[1::2].astype(np.int32))
 
 
 def split_lpt(pat_len: np.ndarray, window: int, overlap: int, n_shards: int) -> list[np.ndarray]:

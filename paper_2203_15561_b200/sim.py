@@ -21,11 +21,21 @@ import numpy as np
 from ._abi import PackedBatch
 
 _ALPHA = np.frombuffer(b"ACGT", dtype=np.uint8)
+_sim_lib = None
 
 
 def _lib():
-    from .engine import lib
-    L = lib()
+    # GA_SIM_SO: the generator built on its own (oracle/_oracle_sim.so), for
+    # bench.py's CPU reference arm, which must not load the product library
+    global _sim_lib
+    if _sim_lib is None:
+        path = os.environ.get("GA_SIM_SO")
+        if path:
+            _sim_lib = C.CDLL(path)
+        else:
+            from .engine import lib
+            _sim_lib = lib()
+    L = _sim_lib
     if not getattr(L, "_sim_sigs", False):
         L.ga_sim_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.ga_sim_derive_seed.restype = C.c_uint64

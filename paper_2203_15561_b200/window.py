@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from . import _abi
 from ._abi import PackedBatch, PackedResults
 
@@ -126,32 +128,62 @@ def _require_gpu_config(cfg: WindowConfig) -> None:
 def outcomes_from_packed(batch: PackedBatch, out: PackedResults,
                          cfg: WindowConfig) -> list[BatchOutcome]:
     """Rebuild the reference's per-slot objects from the C-ABI records
-    (window.py:144-149: failures become ``"{type}: {message}"`` strings)."""
+    (window.py:144-149: failures become ``"{type}: {message}"`` strings).
+
+    Bulk form: the op bytes are decoded to one str and the window distances
+    to one list, each pair slices them; the frozen result objects are filled
+    through their ``__dict__`` (what the generated ``__init__`` stores, minus
+    a per-field ``object.__setattr__``) -- equal objects, several times
+    faster for 10^5 pairs."""
     res = out.results
-    outcomes: list[BatchOutcome] = []
+    n = batch.n_pairs
     status = res["status"].tolist()
-    for q in range(batch.n_pairs):
+    cost = res["cost"].tolist()
+    tcons = res["text_consumed"].tolist()
+    rows = res["rows_computed"].tolist()
+    reads = res["entry_reads"].tolist()
+    writes = res["entry_writes"].tolist()
+    words = res["words_allocated"].tolist()
+    fail = res["fail_window"].tolist()
+    ops_len = res["ops_len"].tolist()
+    ops_off = out.ops_off.tolist()
+    win_off = out.win_off.tolist()
+    nwin = _abi.num_windows(batch.pat_len, cfg.window, cfg.overlap)
+    nwin = nwin.tolist() if n else []
+    if out.ops2:
+        lut = np.frombuffer(b"=XID", dtype=np.uint8)
+        ops_buf = lut[((out.ops[:, None] >> np.array([0, 2, 4, 6], dtype=np.uint8)) & 3)
+                      .reshape(-1)]
+    else:
+        ops_buf = out.ops
+    ops_mv = memoryview(np.ascontiguousarray(ops_buf))  # each CIGAR decoded straight from it
+    dists = out.dists.tolist()
+    new = object.__new__
+    outcomes: list[BatchOutcome] = []
+    append = outcomes.append
+    for q in range(n):
         st = status[q]
         if st == _abi.GA_OK:
-            r = res[q]
-            outcomes.append(BatchOutcome(result=AlignmentResult(
-                cigar=out.cigar(q),
-                cost=int(r["cost"]),
-                text_consumed=int(r["text_consumed"]),
-                window_distances=out.distances(q, int(batch.pat_len[q]), cfg.window, cfg.overlap),
-                counters=AccessCounters(int(r["entry_reads"]), int(r["entry_writes"]),
-                                        int(r["words_allocated"])),
-                rows_computed=int(r["rows_computed"]),
-            )))
+            o, w = ops_off[q], win_off[q]
+            c = new(AccessCounters)
+            c.__dict__.update(entry_reads=reads[q], entry_writes=writes[q],
+                              words_allocated=words[q])
+            r = new(AlignmentResult)
+            r.__dict__.update(cigar=str(ops_mv[o:o + ops_len[q]], "ascii"), cost=cost[q],
+                              text_consumed=tcons[q],
+                              window_distances=tuple(dists[w:w + nwin[q]]), counters=c,
+                              rows_computed=rows[q])
+            b = new(BatchOutcome)
+            b.__dict__.update(result=r, error=None)
+            append(b)
         elif st == _abi.GA_WINDOW_FAILED:
-            exc = WindowFailed(int(res["fail_window"][q]), cfg.k)
-            outcomes.append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
+            exc = WindowFailed(fail[q], cfg.k)
+            append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
         elif st == _abi.GA_EMPTY_PATTERN:
             exc = EmptyPattern("pattern must not be empty")
-            outcomes.append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
+            append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
         else:
-            raise StuckTraceback(
-                f"pair {q}: traceback tripwire fired in window {int(res['fail_window'][q])}")
+            raise StuckTraceback(f"pair {q}: traceback tripwire fired in window {fail[q]}")
     return outcomes
 
 
@@ -181,7 +213,7 @@ def align_batch(pairs: list[tuple[str, str]], cfg: WindowConfig,
     _require_gpu_config(cfg)
     if not pairs:
         return []
-    from .engine import run_batch
-    batch = PackedBatch.from_pairs(pairs)
+    from .engine import pack_pairs, run_batch
+    batch = pack_pairs(pairs)
     out = run_batch(batch, cfg, devices=devices)
     return outcomes_from_packed(batch, out, cfg)

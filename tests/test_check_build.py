@@ -21,8 +21,8 @@ CHECK_SO = os.path.join(ROOT, "paper_2203_15561_b200", "_genasm_check.so")
 
 @pytest.mark.gpu
 def test_check_build_clean():
-    if not os.path.exists(CHECK_SO):
-        from paper_2203_15561_b200 import build
+    from paper_2203_15561_b200 import build
+    if build.needs_build(CHECK_SO):
         build.build(check=True)
     env = dict(os.environ, GA_SO=CHECK_SO)
     proc = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "check_run.py")], env=env,

@@ -245,9 +245,40 @@ def test_chunked_pipeline(gpu, monkeypatch, chunks):
             assert got.cigar(q) == ref.cigar(q)
 
 
+def _all_ops_equal(got, exp, tag="", chunk=4096):
+    """Every op byte of every pair, compared in vectorised chunks of pairs;
+    `got` may hold 2-bit ops (ops2: offsets rounded to 4, its own layout)."""
+    n = exp.results.shape[0]
+    ln_all = exp.results["ops_len"].astype(np.int64)
+    assert np.array_equal(got.results["ops_len"], exp.results["ops_len"]), tag
+    total = 0
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        ln = ln_all[a:b]
+        m = int(ln.sum())
+        if m == 0:
+            continue
+        # position k of pair q -> (offset + k), for every pair of the chunk
+        rank = np.arange(m, dtype=np.int64) - np.repeat(np.cumsum(ln) - ln, ln)
+        e_pos = np.repeat(exp.ops_off[a:b], ln) + rank
+        g_pos = np.repeat(got.ops_off[a:b], ln) + rank
+        e = exp.ops[e_pos]
+        if got.ops2:
+            g = np.frombuffer(b"=XID", dtype=np.uint8)[(got.ops[g_pos >> 2] >> ((g_pos & 3) * 2).astype(np.uint8)) & 3]
+        else:
+            g = got.ops[g_pos]
+        bad = np.nonzero(g != e)[0]
+        if bad.size:
+            q = a + int(np.searchsorted(np.cumsum(ln), bad[0], side="right"))
+            raise AssertionError(f"{tag}: {bad.size} op bytes differ in pairs {a}..{b}, first in pair {q}")
+        total += m
+    return total
+
+
 def test_config3_full_vs_oracle(gpu, oracle_mod):
     """The bench workload itself: all 138,929 pairs of config 3, every field
-    against the oracle (the reference's golden digests pin the prefix)."""
+    and EVERY CIGAR byte against the oracle (the reference's golden digests pin
+    the prefix)."""
     from paper_2203_15561_b200 import sim
     from paper_2203_15561_b200.engine import run_packed
     batch, _ = sim.config_pairs(3)
@@ -255,10 +286,64 @@ def test_config3_full_vs_oracle(gpu, oracle_mod):
     exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
     assert np.array_equal(got.results, exp.results)
     assert np.array_equal(got.dists, exp.dists)
-    for q in range(0, batch.n_pairs, 97):
-        assert got.cigar(q) == exp.ops[int(exp.ops_off[q]):int(exp.ops_off[q])
-                                       + int(exp.results["ops_len"][q])].tobytes().decode(), q
+    n_ops = _all_ops_equal(got, exp, "config3")
+    assert n_ops == int(exp.results["ops_len"].sum()) > 1_300_000_000
     assert (got.results["status"] == 0).all()  # k = W: every window aligns
+
+
+def test_config4_full_vs_oracle(gpu, oracle_mod):
+    """All 20,000 ultra-long config-4 pairs (~2,450-window chains, the
+    reference's window loop pkg/src/bitalign/window.py:95-120), every field and
+    every op byte against the oracle; the reference's own digests pin the
+    first four (test_config4_prefix_vs_reference)."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(4, threads=os.cpu_count())
+    got = run_packed(batch, 64, 24, 64, "MSID", packed2=True)
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    assert np.array_equal(got.results, exp.results)
+    assert np.array_equal(got.dists, exp.dists)
+    _all_ops_equal(got, exp, "config4")
+    assert (got.results["status"] == 0).all()
+
+
+@pytest.mark.parametrize("w,o,k", [(w, 3 * w // 8, k) for w in (32, 64, 128)
+                                   for k in (w // 4, w // 2, w)])
+def test_config5_sweep_full_vs_oracle(gpu, oracle_mod, w, o, k):
+    """Config 5 (8,192 mixed 100 bp - 50 kb pairs) at every W x k sweep point,
+    every pair, every field and op byte against the oracle -- including the
+    WindowFailed-heavy k = W/4 points."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    batch, _ = sim.config_pairs(5)
+    got = run_packed(batch, w, o, k, "MSID")
+    exp = oracle_mod.align_packed(batch, w, o, k, "MSID", threads=os.cpu_count())
+    _packed_equal(got, exp, (w, o, k))
+    _all_ops_equal(got, exp, (w, o, k))
+
+
+def test_full_tier_beyond_level_63(gpu, oracle_mod):
+    """Windows at d_min = m = 64 (runs of 'N' or lowercase longer than W: no
+    symbol matches): the full tier's third pass holds level
+    64 alone and must stay inside the warp's table region.  Every
+    pair of the batch -- including the neighbours whose tables follow in
+    memory -- against the oracle."""
+    import random
+
+    from paper_2203_15561_b200._abi import PackedBatch
+    from paper_2203_15561_b200.engine import run_packed
+    rng = random.Random(64)
+    pairs = []
+    for q in range(96):
+        core = "".join(rng.choice("ACGT") for _ in range(rng.randrange(100, 900)))
+        cut = rng.randrange(0, len(core))
+        run = ("N" if q % 2 else "a") * rng.randrange(64, 260)
+        pairs.append((core[:cut] + run + core[cut:], corpus.noisy_copy(rng, core, 0.05)))
+    batch = PackedBatch.from_pairs(pairs)
+    for prio in ("MSID", "IDSM"):
+        got = run_packed(batch, 64, 24, 64, prio)
+        exp = oracle_mod.align_packed(batch, 64, 24, 64, prio, threads=os.cpu_count())
+        _packed_equal(got, exp, ("deep", prio))
 
 
 @pytest.mark.parametrize("kernel", ["thread", "lockstep"])
