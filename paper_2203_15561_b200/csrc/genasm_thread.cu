@@ -186,7 +186,15 @@ __device__ __noinline__ void fail_pair_ref(const KernelParams& P, int pair, int 
     fail_pair(reinterpret_cast<PairResult*>(P.results), P.dists, P.W, P.O, pair, status, widx, Lp, dst);
 }
 
+#ifdef GA_DEV_FINISH_ATOMIC
+// dev: the round-1 experiment (DESIGN 9) -- a system-scope atomic in finish()
+__device__ unsigned long long g_finished;
+#endif
+
 __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
+#ifdef GA_DEV_FINISH_ATOMIC
+    atomicAdd_system(&g_finished, 1ull);
+#endif
     if (status == 0) {
         PairResult r;
         r.status = 0;

@@ -46,6 +46,12 @@ def main():
         batch, _ = sim.config_pairs(cid, count=count)
         for p in pts:
             cases.append((f"config{cid} {p}", batch, p))
+    import json as _json
+    gold = _json.load(open(os.path.join(ROOT, "tests", "golden", "fuzz.json")))
+    for n, ((w, o, k, prio), pairs) in enumerate(corpus.fuzz_cases(gold["seed"], gold["batches"])):
+        if w <= 64:  # the reference-golden corpus (DESIGN 9: W=32 O=31 among them)
+            cases.append((f"gold{n}", _abi.PackedBatch.from_pairs(pairs),
+                          (w, o, w if k is None else k, prio)))
     for n, ((w, o, k, prio), pairs) in enumerate(corpus.fuzz_cases(5151, 60, pairs_per_batch=24,
                                                                  max_len=2500)):
         if w <= 64:
@@ -63,6 +69,10 @@ def main():
         deep.append((p, corpus.noisy_copy(rng, core, 0.05)))
     for prio in ("MSID", "IDSM"):
         cases.append((f"deep {prio}", _abi.PackedBatch.from_pairs(deep), (64, 24, 64, prio)))
+    # budget-1 windows (O = W - 1): one pattern symbol per window
+    b1, _ = sim.config_pairs(5, count=200)
+    for (w, o) in ((32, 31), (64, 63), (16, 15)):
+        cases.append((f"budget1 w{w}", b1, (w, o, w, "MSID")))
     mismatches = []
     for tag, batch, (w, o, k, prio) in cases:
         if compare(batch, w, o, k, prio):
