@@ -275,9 +275,11 @@ static uint32_t pack_priority(const char* pr) {
 
 // one fused DC+TB launch over device buffers with the given scratch
 static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
-                        const ga_batch_out* out, cudaStream_t st, Scratch* sc) {
+                        const ga_batch_out* out, cudaStream_t st, Scratch* sc,
+                        bool overlapped = false) {
     cudaError_t e;
-    if (!sc->queue && (e = cudaMalloc(&sc->queue, sizeof(unsigned long long))))
+    // [0] the fresh-pair queue, [1] finished pairs (lane-per-pair kernel)
+    if (!sc->queue && (e = cudaMalloc(&sc->queue, 2 * sizeof(unsigned long long))))
         return fail(c, e, "cudaMalloc");
     genasm::KernelParams P{};
     P.codes = in->codes;
@@ -309,7 +311,8 @@ static int launch_batch(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg,
     P.win_off = out->win_off;
     P.dists = out->window_distances;
     P.queue = sc->queue;
-    e = cudaMemsetAsync(sc->queue, 0, sizeof(unsigned long long), st);
+    P.overlapped = overlapped ? 1 : 0;
+    e = cudaMemsetAsync(sc->queue, 0, 2 * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return fail(c, e, "queue reset");
     // tuning knobs (defaults measured on config 3): lanes per pair group, threads per block
     // W <= 64: the lane-per-pair kernel; GA_KERNEL=lockstep forces the
@@ -349,7 +352,7 @@ int ga_edit_distance(ga_ctx* c, const ga_batch_in* in, int32_t semiglobal, int64
     if ((e = c->dp_in.ensure(syms)) || (e = c->dp_meta.ensure(meta)) ||
         (e = c->dp_out.ensure((size_t)n * 8)))
         return fail(c, e, "cudaMalloc (edit distance)");
-    if (!c->scratch.queue && (e = cudaMalloc(&c->scratch.queue, sizeof(unsigned long long))))
+    if (!c->scratch.queue && (e = cudaMalloc(&c->scratch.queue, 2 * sizeof(unsigned long long))))
         return fail(c, e, "cudaMalloc");
     char* m = (char*)c->dp_meta.ptr;
     int64_t* pat_off = (int64_t*)m;
@@ -645,7 +648,7 @@ static int align_chunks(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, 
         dout.win_off = d64 + 3 * m;
         dout.window_distances = (uint8_t*)S.dists.ptr;
         dout.win_capacity = nwin;
-        const int rc = launch_batch(c, &din, cfg, &dout, sk, &S.scratch);
+        const int rc = launch_batch(c, &din, cfg, &dout, sk, &S.scratch, chunks > 1);
         if (rc) return rc;
         launches += c->last_shape.launches;
         if (out->ops2) {

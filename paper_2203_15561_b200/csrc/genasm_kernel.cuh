@@ -50,6 +50,8 @@ struct KernelParams {
     int64_t overflow_words_per_group;
     uint32_t* band;            // per-warp global band tables
     unsigned long long* queue; // atomic pair counter
+    int32_t overlapped;        // 1: other launches share the GPU (pipeline chunks): keep no
+                               // idle warps resident (lane-per-pair kernel)
 };
 
 struct PairResult {  // == ga_pair_result

@@ -32,6 +32,8 @@ namespace genasm {
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
 __device__ unsigned long long g_thread_stats[12];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB
+// per pair: first window started, finished (globaltimer ns), full-tier windows
+__device__ unsigned long long g_pair_t[3][262144];
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
 #define GA_STAT(k, v) ((void)0)
@@ -152,6 +154,13 @@ struct Lane {
 
 __device__ __forceinline__ void fresh_pair(const KernelParams& P, Lane& L, int pair) {
     L.pair = pair;
+#ifdef GA_THREAD_STATS
+    if (pair < 262144) {
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        atomicMin(&g_pair_t[0][pair], tnow);
+    }
+#endif
     L.Lp = P.pat_len[pair];
     L.Lt = P.txt_len[pair];
     L.pat = P.pat_off[pair];
@@ -210,6 +219,13 @@ __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int statu
     } else {
         fail_pair_ref(P, L.pair, status, L.widx, L.Lp, L.dst);
     }
+#ifdef GA_THREAD_STATS
+    if (L.pair < 262144) {
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        g_pair_t[1][L.pair] = tnow;
+    }
+#endif
     L.pair = -1;
 }
 
@@ -410,7 +426,20 @@ struct HandList {
     int32_t* list;      // pair ids by ticket, -1 until published
     unsigned* count;    // tickets handed out to producers
     unsigned* claim;    // tickets taken by consumers
+    unsigned* finished; // pairs finished (any status)
+    unsigned* sm_claims;  // per SM (by %smid): fresh pairs taken / warps lingering
+    unsigned* linger;
+    int sm_share;       // fresh pairs per SM when pairs are fewer than lanes (else 0)
+    int linger_cap;     // warps per SM that stay to serve hand-overs (else 0)
 };
+
+// %smid numbering need not be contiguous: per-SM arrays have kSmSlots entries
+constexpr int kSmSlots = 1024;
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r & (kSmSlots - 1);
+}
 
 __device__ __forceinline__ void hand_over(const KernelParams& P, Lane& L, const HandList& H) {
     PairResult* r = reinterpret_cast<PairResult*>(P.results) + L.pair;
@@ -577,6 +606,9 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
         GA_STAT(11, clock64() - c1);
 #endif
         if (lane == owner) {
+#ifdef GA_THREAD_STATS
+            if (L.pair < 262144) g_pair_t[2][L.pair] += 1;
+#endif
             L.nops = nops;
             if (ok) book(P, L, w, d_min, o);
             else finish(P, L, 3);
@@ -634,6 +666,12 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
 #define GA_THREAD_MINB (512 / GA_TBLOCK)  // blocks per SM the register budget must allow
 #endif
 
+// kShare: the launch has fewer pairs than lanes and the GPU to itself -- an
+// equal share of the pairs per SM, and idle warps that stay to serve the
+// hand-over list.  A separate instance, so the common case's code and
+// register allocation do not carry it (the shared instance measured 4 %
+// slower on config 3).
+template <bool kShare>
 __global__ void __launch_bounds__(kTBlock, GA_THREAD_MINB)
 genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H) {
     const int lane = threadIdx.x & 31;
@@ -648,18 +686,29 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     uint2* pmt = s_pm[threadIdx.x >> 5];
     const unsigned lt = lanemask_lt();
     bool exhausted = false;
+    bool capped = false, uncapped = false;  // this SM's share of the pairs is taken / ignored
+    unsigned long long cap_q = ~0ull, cap_t = 0;  // queue position last seen while capped, when
     Lane L;
     L.pair = -1;
     for (;;) {
         // ---- free lanes take fresh pairs from the global longest-first queue ----
         unsigned freem = __ballot_sync(FULL, L.pair < 0);
         if (freem && !exhausted) {
-            const int cnt = __popc(freem);
+            int cnt = __popc(freem);
             unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(P.queue, (unsigned long long)cnt);
+            if (lane == 0) {
+                if (kShare && H.sm_share && !uncapped) {  // an equal share per SM
+                    const int had = (int)atomicAdd(H.sm_claims + smid(), (unsigned)cnt);
+                    const int left = H.sm_share - had;
+                    cnt = left < 0 ? 0 : (left < cnt ? left : cnt);
+                }
+                base = cnt ? atomicAdd(P.queue, (unsigned long long)cnt) : 0ull;
+            }
+            cnt = __shfl_sync(FULL, cnt, 0);
             base = __shfl_sync(FULL, base, 0);
-            if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
-            if (L.pair < 0) {
+            if (kShare && cnt == 0) capped = true;  // this SM's share is taken (the queue may not be)
+            else if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
+            if (L.pair < 0 && (int)__popc(freem & lt) < cnt) {
                 const uint64_t idx = base + __popc(freem & lt);
                 if (idx < (uint64_t)P.n_pairs) {
                     fresh_pair(P, L, P.order ? P.order[idx] : (int)idx);
@@ -670,6 +719,29 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         const unsigned active = __ballot_sync(FULL, L.pair >= 0);
         if (!active) {
             if (exhausted) break;
+            if (kShare && capped) {
+                // The share only balances the start.  An SM that never runs a
+                // block of this launch would leave its share unclaimed, so a
+                // capped warp with nothing to do stops once the queue is
+                // empty, and takes what is left if the queue stands still for
+                // 200 us (nobody else is claiming it).
+                unsigned long long q = 0, tnow = 0;
+                if (lane == 0) {
+                    q = *(volatile unsigned long long*)P.queue;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                }
+                q = __shfl_sync(FULL, q, 0);
+                tnow = __shfl_sync(FULL, tnow, 0);
+                if (q >= (unsigned long long)P.n_pairs) break;
+                if (q != cap_q) {
+                    cap_q = q;
+                    cap_t = tnow;
+                } else if (tnow - cap_t > 200000ull) {
+                    uncapped = true;
+                    capped = false;
+                }
+                __nanosleep(2000);
+            }
             continue;
         }
 
@@ -731,6 +803,13 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         }
     }
 #endif
+    // P.queue[1] counts the warps past their own pairs (P.queue[0] is the
+    // fresh-pair queue): hand-overs come only from warps before this point.
+    // (A count of finished pairs instead -- one atomic per pair -- measured
+    // 5 ms slower on config 3.)
+    if (kShare && lane == 0) atomicAdd(P.queue + 1, 1ull);
+    bool lingering = false;
+    unsigned nap = 256;
     // ---- handed-over pairs: a warp out of pairs claims the published ones,
     // one at a time, and finishes each with all lanes, every window in the
     // full tier (up to k).  It claims only while unclaimed tickets exist and
@@ -750,7 +829,29 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             }
         }
         ticket = __shfl_sync(FULL, ticket, 0);
-        if (ticket < 0) break;
+        if (ticket < 0) {
+            // Nothing published.  Up to linger_cap warps per SM stay (while
+            // pairs remain unfinished) so a pair handed over later -- an
+            // unrelated or desynchronised pair whose every window needs the
+            // full tier -- is taken at once instead of when its producer's
+            // other pairs are done; the rest leave the SM.
+            if (!kShare) break;
+            if (!lingering) {
+                int stay = 0;
+                if (lane == 0 && H.linger_cap)
+                    stay = (int)atomicAdd(H.linger + smid(), 1u) < H.linger_cap;
+                if (!__shfl_sync(FULL, stay, 0)) break;
+                lingering = true;
+            }
+            // every warp past its own pairs: no hand-over can come any more
+            unsigned long long past = 0;
+            if (lane == 0) past = *(volatile unsigned long long*)(P.queue + 1);
+            if (__shfl_sync(FULL, past, 0) >= (unsigned long long)gridDim.x * kWarps) break;
+            __nanosleep(nap);
+            nap = nap < 4096 ? 2 * nap : nap;
+            continue;
+        }
+        nap = 256;
         int pair = -1;
         for (;;) {  // the producer publishes right after taking the slot
             if (lane == 0) pair = *(volatile int32_t*)(H.list + ticket);
@@ -775,7 +876,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     KernelParams P = base;
     int per_sm = 0;
     cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, genasm_thread_kernel, kTBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, genasm_thread_kernel<false>, kTBlock, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const char* cap_env = getenv("GA_WARPS_PER_SM");
@@ -786,9 +887,22 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     if (bcap >= 1 && per_sm > bcap) per_sm = bcap;
     // every SM equally loaded; lanes pull pairs from the global queue
     const int64_t resident = (int64_t)num_sms * per_sm * kTBlock;
+    // Pairs at least as many as lanes: every warp resident, lanes refill from
+    // the queue.  Fewer, with the GPU to itself (the device call, a one-chunk
+    // host call): still every warp, an equal share of the pairs per SM (by
+    // %smid), and the warps without pairs serve the hand-over list
+    // (genasm_thread_kernel<true>; config 4: 106 -> 83-91 ms).  Fewer in an
+    // overlapped pipeline chunk: as many lanes as pairs.
+    const int sm_share = P.n_pairs < resident && !P.overlapped
+                             ? (int)((P.n_pairs + num_sms - 1) / num_sms) : 0;
     const int64_t lanes = P.n_pairs < resident ? P.n_pairs : resident;
-    int grid = (int)((lanes + kTBlock - 1) / kTBlock);
-    if (grid < 1) grid = 1;
+    const int grid = sm_share ? num_sms * per_sm : (int)((lanes + kTBlock - 1) / kTBlock > 0
+                                                         ? (lanes + kTBlock - 1) / kTBlock : 1);
+    // idle warps kept to serve hand-overs: only when this launch has the GPU
+    // to itself (pipeline chunks overlap each other's launches, and a warp
+    // lingering in one holds a slot the next needs: e2e 2.64 -> 2.07 M/s)
+    const char* lc = getenv("GA_LINGER");
+    const int linger_cap = sm_share && !P.overlapped ? (lc ? atoi(lc) : 4) : 0;
     // scratch: per-warp tables | bit-planes (one word per 64 symbols per
     // plane, plus a word of slack)
     const size_t warps = (size_t)grid * kWarps;
@@ -796,7 +910,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     const int64_t pw = (P.codes_len + 63) / 64 + 1;
     const size_t plane_total = ((size_t)pw * 3 * 2 + 63) & ~(size_t)63;
     const size_t list_words = ((size_t)P.n_pairs + 63 + 64) & ~(size_t)63;
-    const size_t need = band_words + plane_total + list_words;
+    const size_t need = band_words + plane_total + list_words + 2 * kSmSlots;
     if (need > *cap || !*scratch) {
         if (*scratch) cudaFree(*scratch);
         *scratch = nullptr;
@@ -819,11 +933,17 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     H.list = reinterpret_cast<int32_t*>(*scratch + band_words + plane_total);
     H.count = reinterpret_cast<unsigned*>(H.list + (((size_t)P.n_pairs + 63) & ~(size_t)63));
     H.claim = H.count + 1;
+    H.sm_claims = *scratch + band_words + plane_total + list_words;
+    H.linger = H.sm_claims + kSmSlots;
+    H.sm_share = sm_share;
+    H.linger_cap = linger_cap;
+    if ((e = cudaMemsetAsync(H.sm_claims, 0, 2 * kSmSlots * 4, stream))) return e;
     if ((e = cudaMemsetAsync(H.list, 0xff, (size_t)P.n_pairs * 4, stream))) return e;
     // the tracebacks write only the ops that are not '='
     if ((e = cudaMemsetAsync(P.ops, '=', (size_t)P.ops_capacity, stream))) return e;
     if ((e = cudaMemsetAsync(H.count, 0, 2 * sizeof(unsigned), stream))) return e;
-    genasm_thread_kernel<<<grid, kTBlock, 0, stream>>>(P, band, H);
+    if (sm_share) genasm_thread_kernel<true><<<grid, kTBlock, 0, stream>>>(P, band, H);
+    else genasm_thread_kernel<false><<<grid, kTBlock, 0, stream>>>(P, band, H);
     shape->grid = grid;
     shape->block = kTBlock;
     shape->smem_bytes = 0;
@@ -852,6 +972,14 @@ extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
     if (reset) {
         unsigned long long z[12] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
+        static unsigned long long pz[3][262144];
+        for (int i = 0; i < 262144; ++i) pz[0][i] = ~0ull;
+        cudaMemcpyToSymbol(genasm::g_pair_t, pz, sizeof pz);
     }
+}
+extern "C" void ga_debug_pair_times(unsigned long long* out, int n) {
+    for (int k = 0; k < 3; ++k)
+        cudaMemcpyFromSymbol(out + (size_t)k * n, genasm::g_pair_t, sizeof(unsigned long long) * n,
+                             sizeof(unsigned long long) * 262144 * k);
 }
 #endif

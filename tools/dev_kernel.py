@@ -60,6 +60,22 @@ def main():
         st.synchronize()
         times.append(a.elapsed_time(b))
     r = res.cpu().numpy().view(_abi.RESULT_DTYPE)
+    if hasattr(L, "ga_debug_pair_times") and n <= 262144:
+        pt = np.zeros(3 * n, np.uint64)
+        L.ga_debug_pair_times(pt.ctypes.data_as(C.c_void_p), n)
+        t0 = pt[:n].min()
+        st_ms = (pt[:n] - t0) / 1e6
+        fin_ms = (pt[n:2 * n] - t0) / 1e6
+        full = pt[2 * n:].astype(np.int64)
+        q = [0, 1, 10, 50, 90, 99, 100]
+        print("pair start ms pct " + " ".join(f"{p}:{np.percentile(st_ms, p):.1f}" for p in q))
+        print("pair finish ms pct " + " ".join(f"{p}:{np.percentile(fin_ms, p):.1f}" for p in q))
+        print("full-tier windows per pair pct " + " ".join(f"{p}:{np.percentile(full, p):.0f}" for p in q))
+        slow = np.argsort(-fin_ms)[:8]
+        print("slowest pairs (id, finish ms, full-tier windows):",
+              [(int(i), round(float(fin_ms[i]), 1), int(full[i])) for i in slow])
+        np.savez_compressed(os.path.join("gpurun_out", f"pairtimes_r1_cfg{cfg_id}.npz"),
+                            start=st_ms, fin=fin_ms, full=full)
     if hasattr(L, "ga_debug_thread_stats"):
         st = np.zeros(12, np.uint64)
         L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
