@@ -187,19 +187,15 @@ __device__ __noinline__ void fail_pair(PairResult* results, uint8_t* dists, int 
     results[pair] = r;
 }
 
-// Taking the parameters by reference puts a copy of them in local memory for
-// the whole kernel (the LDLs hit L1); measured 1.5 % faster on config 3 than
-// passing plain values (38.2 vs 38.8 ms: 107 registers instead of 115).
-__device__ __noinline__ void fail_pair_ref(const KernelParams& P, int pair, int status, int widx, int Lp,
-                                           int64_t dst) {
-    fail_pair(reinterpret_cast<PairResult*>(P.results), P.dists, P.W, P.O, pair, status, widx, Lp, dst);
-}
-
-#ifdef GA_DEV_FINISH_ATOMIC
-// dev: the round-1 experiment (DESIGN 9) -- a system-scope atomic in finish()
-__device__ unsigned long long g_finished;
-#endif
-
+// The launch parameters are never taken by reference by an out-of-line
+// function (fail_pair gets plain values).  A reference makes the compiler keep
+// a copy of them in local memory for the whole kernel; with that copy, a
+// shared-memory carry added to the full tier's second pass (coop_dc) produced
+// wrong window geometry for W = 32, O = 31 -- window_of() saw budget 1 on
+// final windows, pairs ran past their pattern -- reproducibly (nvcc 12.9,
+// sm_100a; tools/dbg_w32.py), and the same code with values passed was
+// correct.  The by-reference form measured 1.5 % faster on config 3; it is not
+// worth a code-shape-dependent miscompile (DESIGN 9).
 __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
 #ifdef GA_DEV_FINISH_ATOMIC
     atomicAdd_system(&g_finished, 1ull);
@@ -217,7 +213,8 @@ __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int statu
         r.words_allocated = L.words;
         reinterpret_cast<PairResult*>(P.results)[L.pair] = r;
     } else {
-        fail_pair_ref(P, L.pair, status, L.widx, L.Lp, L.dst);
+        fail_pair(reinterpret_cast<PairResult*>(P.results), P.dists, P.W, P.O, L.pair, status,
+                  L.widx, L.Lp, L.dst);
     }
 #ifdef GA_THREAD_STATS
     if (L.pair < 262144) {
