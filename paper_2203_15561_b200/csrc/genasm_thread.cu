@@ -346,13 +346,75 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
     return (uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), src) << 32 | __shfl_sync(FULL, (uint32_t)v, src);
 }
 
-// Full tier, the whole warp on one window: lane q computes level d0+q of
-// full-width rows (distance.py:125-149, two 32-bit words) as a wavefront --
-// at step s it evaluates column j = s - q + 1, taking R[d-1][j] from lane
-// q-1 by shuffle (lane q-1 produced it the step before; lane 0 reads the row
-// lane 31 stored in the previous pass) -- and stores every row to
-// tab[full_index(d, j)].  Passes of 32 levels run until a level <= k has
-// R[d][n] bit m-1 active or the passes cover kmax.  Returns that d_min, or -1.
+// One pass of the full tier's wavefront: lane q computes level d = d0+q of
+// full-width rows (distance.py:125-149, two 32-bit words); at step s it
+// evaluates column j = s - q + 1, taking R[d-1][j] from lane q-1 by shuffle
+// (lane q-1 produced it the step before).  Lane 0 of a later pass (kCarry)
+// reads R[d0-1][j] -- stored by lane 31 in the pass before -- from the table,
+// a few steps ahead; the first pass has no carry and holds level 0.  Rows go
+// to out[s * 32] (step-major, full_index).  The steps are branch-free: a lane
+// outside 1 <= j <= n computes and discards.  Measured on the warp's own
+// (tools/coop_bench.cu, cycles per 95-step pass, one warp per SM partition):
+// a carry load in the first pass's steps, even predicated off, 11.5 k against
+// 6-8 k without; the carry through shared memory instead (lane 31 stores,
+// lane 0 loads) 13.4-13.9 k; the next step's mismatch words loaded a step
+// ahead 9.5 k against 8.0 k.
+template <bool kCarry>
+__device__ __forceinline__ void coop_pass(int m, int n, int d, uint64_t* out, const uint2* pmt,
+                                          int q, uint32_t& cl, uint32_t& ch) {
+    using namespace thr;
+    constexpr int kAhead = 4;  // carry rows in flight
+    const uint64_t a0 = d > 0 ? init_row64(m, d - 1) : 0ull;  // R[d-1][0]
+    uint32_t al = (uint32_t)a0, ah = (uint32_t)(a0 >> 32);
+    uint32_t ol = 0, oh = 0;  // this lane's last output
+    const bool lvl0 = !kCarry && q == 0;
+    const bool keep = d <= m;  // d_min <= m: no level above m is ever read
+    const int S = n + kFullLevels - 1;
+    // lane 0 of a later pass: R[d0-1][s+1], stored by lane 31 of the pass
+    // before at its step s+31, i.e. at cin[s * 32]
+    const uint64_t* cin = out - 96 * kFullLevels + (kFullLevels - 1) * kFullLevels + (kFullLevels - 1);
+    uint64_t cv[kAhead];
+    if (kCarry) {
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) cv[u] = q == 0 && u < n ? cin[u * kFullLevels] : 0ull;
+    }
+#pragma unroll 2
+    for (int s = 0; s < S; ++s) {
+        uint32_t bl = __shfl_up_sync(FULL, ol, 1), bh = __shfl_up_sync(FULL, oh, 1);
+        const int j = s - q + 1;
+        const bool valid = (unsigned)(j - 1) < (unsigned)n;
+        if (kCarry) {
+            bl = q == 0 ? (uint32_t)cv[0] : bl;
+            bh = q == 0 ? (uint32_t)(cv[0] >> 32) : bh;
+#pragma unroll
+            for (int u = 0; u + 1 < kAhead; ++u) cv[u] = cv[u + 1];
+            cv[kAhead - 1] = q == 0 && s + kAhead < n ? cin[(size_t)(s + kAhead) * kFullLevels] : 0ull;
+        }
+        const uint2 pm = pmt[valid ? j - 1 : 0];
+        const uint32_t xl = cl << 1, xh = shl1_hi(cl, ch);
+        uint32_t nl = and3(orand(xl, pm.x, al << 1), bl << 1, al);
+        uint32_t nh = and3(orand(xh, pm.y, shl1_hi(al, ah)), shl1_hi(bl, bh), ah);
+        if (!kCarry) {  // level 0: the match edge only
+            nl = lvl0 ? (xl | pm.x) : nl;
+            nh = lvl0 ? (xh | pm.y) : nh;
+        }
+        al = valid ? bl : al;
+        ah = valid ? bh : ah;
+        cl = valid ? nl : cl;
+        ch = valid ? nh : ch;
+        ol = cl;
+        oh = ch;
+        if (valid && keep &&
+            GA_ASSERT((d >> 5) * (96 * kFullLevels) + s * kFullLevels + q < kBandWordsPerWarp / 2, 7,
+                      d, j))
+            out[(size_t)s * kFullLevels] = (uint64_t)nh << 32 | nl;
+    }
+}
+
+// Full tier, the whole warp on one window: passes of 32 levels (coop_pass),
+// rows stored to tab[full_index(d, j)], until a level <= k has R[d][n] bit
+// m-1 active or the passes cover kmax.  Returns that d_min, or -1.  pmt: the
+// window's mismatch words (64, shared memory).
 __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes& tp, int m, int n,
                                        int K, int kmax, uint64_t* tab, uint2* pmt, int lane) {
     using namespace thr;
@@ -376,41 +438,13 @@ __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes&
     // pass used to overrun it)
     for (int d0 = 0; d0 <= K && d0 <= kmax && d0 <= m; d0 += kFullLevels) {
         const int d = d0 + q;
-        uint64_t c = init_row64(m, d);                    // R[d][j-1]
-        uint64_t a = d > 0 ? init_row64(m, d - 1) : 0ull; // R[d-1][j-1]
-        uint32_t ol = 0, oh = 0;                          // this lane's last output
-        for (int s = 0; s < n + kFullLevels - 1; ++s) {
-            uint32_t bl = __shfl_up_sync(FULL, ol, 1), bh = __shfl_up_sync(FULL, oh, 1);
-            const int j = s - q + 1;
-            if (j >= 1 && j <= n) {
-                if (q == 0 && d0 > 0) {  // R[d0-1][j]: the previous pass's last level
-                    const uint64_t v = tab[full_index(d0 - 1, j)];
-                    bl = (uint32_t)v;
-                    bh = (uint32_t)(v >> 32);
-                }
-                const uint2 pmv = pmt[j - 1];
-                const uint32_t pml = pmv.x, pmh = pmv.y;
-                const uint32_t cl = (uint32_t)c, ch = (uint32_t)(c >> 32);
-                const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
-                const uint32_t xl = cl << 1, xh = shl1_hi(cl, ch);
-                uint32_t nl, nh;
-                if (d == 0) {  // level 0: the match edge only
-                    nl = xl | pml;
-                    nh = xh | pmh;
-                } else {
-                    nl = and3(orand(xl, pml, al << 1), bl << 1, al);
-                    nh = and3(orand(xh, pmh, shl1_hi(al, ah)), shl1_hi(bl, bh), ah);
-                }
-                a = (uint64_t)bh << 32 | bl;
-                c = (uint64_t)nh << 32 | nl;
-                ol = nl;
-                oh = nh;
-                if (d <= m && GA_ASSERT(full_index(d, j) < kBandWordsPerWarp / 2, 7, d, j))
-                    tab[full_index(d, j)] = c;
-            }
-        }
-        __syncwarp();  // rows are read by the next pass's lane 0 and by the traceback
-        const bool hit = d <= K && d <= m && !((c >> (m - 1)) & 1ull);
+        const uint64_t c0 = init_row64(m, d);  // R[d][0]
+        uint32_t cl = (uint32_t)c0, ch = (uint32_t)(c0 >> 32);
+        uint64_t* out = tab + (size_t)(d0 >> 5) * (96 * kFullLevels) + q;
+        if (d0 == 0) coop_pass<false>(m, n, d, out, pmt, q, cl, ch);
+        else coop_pass<true>(m, n, d, out, pmt, q, cl, ch);
+        __syncwarp();  // rows are read by the next pass and the traceback
+        const bool hit = d <= K && d <= m && !(((uint64_t)ch << 32 | cl) >> (m - 1) & 1ull);
         const unsigned hm = __ballot_sync(FULL, hit);
         if (hm) return d0 + __ffs(hm) - 1;
     }
