@@ -477,7 +477,12 @@ static int align_chunks(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, 
     // ---- chunk plan: consecutive pairs, pipelined over kSlots slots.  Chunking
     // needs output offsets that grow with the input index (the prefix-sum
     // layout every caller in this package uses); otherwise one chunk. ----
-    int chunks = env_int("GA_CHUNKS", (int)std::min<int64_t>(4, std::max<int64_t>(1, n / 12000)));
+    // One chunk per ~512 MB of sequence, at most 4: below that a batch's copy
+    // is short against its kernel and pipelining gains nothing; above, the
+    // copy of chunk k+1 hides under chunk k's kernel.
+    int64_t seq_bytes = 0;
+    for (int64_t q = 0; q < n; ++q) seq_bytes += (int64_t)in->pat_len[q] + in->txt_len[q];
+    int chunks = env_int("GA_CHUNKS", (int)std::min<int64_t>(4, std::max<int64_t>(1, (seq_bytes + (256 << 20)) >> 29)));
     if (chunks < 1) chunks = 1;
     if (chunks > n) chunks = (int)n;
     for (int64_t q = 1; q < n && chunks > 1; ++q)
@@ -497,10 +502,12 @@ static int align_chunks(ga_ctx* c, const ga_batch_in* in, const ga_config* cfg, 
             if (v > 0) wts.push_back(v);
             s = *end == ',' ? end + 1 : end;
         }
-        if (!plan && chunks == 4 && n >= 72000) {
-            // measured on config 3 (tools/e2e_sweep.py): eight chunks, one slot
-            // each, the first and last half-size
-            wts = {1, 2, 2, 2, 2, 2, 2, 1};
+        if (!plan && chunks >= 3) {
+            // twice the chunks, the first and last half-size: the kernels start
+            // on a small first copy and the drain after the last copy is short
+            // (tools/e2e_sweep.py on config 3: equal 4 chunks 71.5 ms, this 66.4)
+            wts.assign((size_t)(2 * chunks), 2.0);
+            wts.front() = wts.back() = 1.0;
         }
         if (wts.size() < 2 || (int64_t)wts.size() > n) wts.assign((size_t)chunks, 1.0);
         if (chunks == 1) wts.assign(1, 1.0);

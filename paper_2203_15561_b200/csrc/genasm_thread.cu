@@ -649,6 +649,23 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
     return false;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Idle for about ns nanoseconds.  __nanosleep alone returns far earlier than
+// asked: a config-4 profile had the idle warps' poll loop at 40 % of all
+// executed instructions (about ten polls per microsecond per warp), issue
+// slots taken from the warps still aligning.
+__device__ __forceinline__ void idle_ns(unsigned long long ns) {
+    const unsigned long long t0 = globaltimer();
+    do {
+        __nanosleep(1000);
+    } while (globaltimer() - t0 < ns);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -771,7 +788,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
                     uncapped = true;
                     capped = false;
                 }
-                __nanosleep(2000);
+                idle_ns(2000);
             }
             continue;
         }
@@ -840,7 +857,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     // 5 ms slower on config 3.)
     if (kShare && lane == 0) atomicAdd(P.queue + 1, 1ull);
     bool lingering = false;
-    unsigned nap = 256;
+    unsigned nap = 250;
     // ---- handed-over pairs: a warp out of pairs claims the published ones,
     // one at a time, and finishes each with all lanes, every window in the
     // full tier (up to k).  It claims only while unclaimed tickets exist and
@@ -878,11 +895,11 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             unsigned long long past = 0;
             if (lane == 0) past = *(volatile unsigned long long*)(P.queue + 1);
             if (__shfl_sync(FULL, past, 0) >= (unsigned long long)gridDim.x * kWarps) break;
-            __nanosleep(nap);
-            nap = nap < 4096 ? 2 * nap : nap;
+            idle_ns(nap);
+            nap = nap < 4000 ? 2 * nap : nap;
             continue;
         }
-        nap = 256;
+        nap = 250;
         int pair = -1;
         for (;;) {  // the producer publishes right after taking the slot
             if (lane == 0) pair = *(volatile int32_t*)(H.list + ticket);
