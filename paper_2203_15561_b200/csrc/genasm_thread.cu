@@ -346,6 +346,152 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
     return (uint64_t)__shfl_sync(FULL, (uint32_t)(v >> 32), src) << 32 | __shfl_sync(FULL, (uint32_t)v, src);
 }
 
+// ---- lane groups: the latency path for batches far smaller than the
+// resident lanes (genasm_thread_kernel<false, true>).  Each half-warp owns one
+// pair; lane q of the group computes band level q (0..15) of every column as
+// a wavefront -- at step s it evaluates column j = s - q + 1, R[q-1][j] from
+// lane q-1 by shuffle -- so a window's DC takes n + 15 steps of one level
+// each instead of n columns of 16 levels on one lane.  The window's band
+// table is in shared memory, [column][level] unrotated (the band tier's
+// exactness argument needs no rotation; rotating levels 8..15 only served the
+// pairing of dc_band), and the group's leader (lane 0 / 16) traces back from
+// it alone with tb_band. ----
+constexpr int kGroupLanes = 16;
+constexpr int kGroupTabWords = 64 * thr::kFastLevels + 16;  // + 16: the two groups' banks differ
+
+struct GroupTab {
+    const uint32_t* base;  // [column - 1][level]
+#ifdef GA_CHECK
+    int jlo, jhi;
+    mutable bool bad;
+#endif
+    __device__ __forceinline__ uint32_t get(int k, int c) const {
+#ifdef GA_CHECK
+        if (!GA_ASSERT(c >= jlo && c <= jhi && k >= 0 && k < thr::kFastLevels, 1, c, k)) {
+            bad = true;
+            return 0xffffffffu;
+        }
+#endif
+        return base[(c - 1) * thr::kFastLevels + k];
+    }
+    __device__ __forceinline__ int wi(int e) const { return e; }
+    __device__ __forceinline__ uint32_t bit(uint32_t w, int e, int b) const {
+        return (w >> (b & 31)) & 1u;
+    }
+};
+
+// mismatch word of column j (1..n) in the window's band coordinates
+// (dc_band's two column ranges in one)
+__device__ __forceinline__ uint32_t band_pm(const thr::Planes& pp, const thr::Planes& tp, int m,
+                                            int n, int j) {
+    const int oj = m - n - 16 + j;
+    if (oj <= 0) {
+        const int sh = -oj;  // virtual bits at the bottom of the band
+        const uint32_t valid = sh < 32 ? ~0u << sh : 0u;
+        return thr::pm_word((uint32_t)(pp.b0 << sh), (uint32_t)(pp.b1 << sh), (uint32_t)(pp.bn << sh),
+                            tp, j - 1) & valid;
+    }
+    return thr::pm_word((uint32_t)(pp.b0 >> oj), (uint32_t)(pp.b1 >> oj), (uint32_t)(pp.bn >> oj), tp,
+                        j - 1);
+}
+
+// One band-tier window per group (all 32 lanes call it; a group without a
+// pair idles through the shared steps).  The leader's return: WIN_HARD (state
+// untouched) if d_min > 15 and k allows more; otherwise the window is booked.
+__device__ __forceinline__ int group_window(const KernelParams& P, Lane& L, uint32_t* gtab,
+                                            uint32_t* gpm, int lane) {
+    using namespace thr;
+    const int q = lane & (kGroupLanes - 1);
+    const int lead = lane & ~(kGroupLanes - 1);
+    const int K = P.k;
+    Win w{};
+    int run = 0;  // 1: the group computes a DC this step
+    if (q == 0 && L.pair >= 0) {
+        w = window_of(P, L);
+        run = 1;
+        if (w.n == 0) {  // R[d][0] = init(m, d) solves iff d >= m (band_window)
+            run = 0;
+            if (w.m > K) {
+                finish(P, L, 1);
+            } else {
+                const int take = w.m < w.budget ? w.m : w.budget;
+                uint8_t* ops = P.ops + L.ops;
+                for (int u = 0; u < take; ++u) ops[L.nops + u] = 'I';
+                L.nops += take;
+                TbOut o;
+                o.consumed = o.wcost = take;
+                o.tcons = 0;
+                o.reads = 0;
+                book(P, L, w, w.m, o);
+            }
+        }
+    }
+    run = __shfl_sync(FULL, run, lead);
+    // (every lane of the warp runs each shuffle: no shuffle under a condition)
+    const int m = __shfl_sync(FULL, w.m, lead);
+    const int wn = __shfl_sync(FULL, w.n, lead);
+    const int n = run ? wn : 0;
+    const int budget = __shfl_sync(FULL, w.budget, lead);
+    const int64_t pat_at = (int64_t)shfl64((uint64_t)(L.pat + w.p), lead);
+    const int64_t txt_at = (int64_t)shfl64((uint64_t)(L.txt + L.t), lead);
+    Planes pp{}, tp{};
+    if (run) {
+        pp = load_planes_bits(P.planes, P.plane_words, pat_at, m);
+        tp = load_planes_bits(P.planes, P.plane_words, txt_at, n);
+        for (int x = q; x < n; x += kGroupLanes) gpm[x] = band_pm(pp, tp, m, n, x + 1);
+    }
+    const int jstore = band_jstore(n, budget);
+    __syncwarp();  // mismatch words in; the previous window's table is no longer read
+    // the wavefront: lane q holds level q
+    const int o0 = m - n - 16;
+    uint32_t c = init_band(m, q, o0);                     // R[q][j-1]
+    uint32_t a = q > 0 ? init_band(m, q - 1, o0) : 0u;    // R[q-1][j-1]
+    uint32_t out = c;
+    const int S = __reduce_max_sync(FULL, run ? n + kGroupLanes - 1 : 0);
+    for (int s = 0; s < S; ++s) {
+        const uint32_t b = __shfl_up_sync(FULL, out, 1, kGroupLanes);  // R[q-1][j]
+        const int j = s - q + 1;
+        const bool valid = (unsigned)(j - 1) < (unsigned)n;
+        const uint32_t pm = gpm[valid ? j - 1 : 0];
+        const uint32_t g = and3(orand(c, pm, a), rotr1(a), rotl1(b));
+        const uint32_t nc = q == 0 ? (c | pm) : g;
+        a = valid ? b : a;
+        c = valid ? nc : c;
+        out = c;
+        if (valid && j >= jstore) gtab[(j - 1) * thr::kFastLevels + q] = c;
+    }
+    __syncwarp();  // the table is complete
+    // levels with R[d][n] bit m-1 (band bit 15) active
+    const unsigned okv = __ballot_sync(FULL, run && !((c >> 15) & 1u));
+    int r = WIN_NEXT;
+    if (q == 0 && run) {
+        uint32_t okm = (okv >> lead) & 0xffffu;
+        const int lim = K < 15 ? K : 15;
+        okm &= (2u << lim) - 1u;
+        if (!okm) {
+            if (K <= 15) finish(P, L, 1);
+            else r = WIN_HARD;
+        } else {
+            const int d_min = __ffs(okm) - 1;
+            GroupTab gt{gtab};
+#ifdef GA_CHECK
+            gt.jlo = jstore;
+            gt.jhi = n;
+            gt.bad = false;
+#endif
+            TbOut o;
+            bool ok = tb_band<false>(gt, pp, tp, m, n, d_min, budget, P.prio_lut, P.ops + L.ops,
+                                     L.nops, o);
+#ifdef GA_CHECK
+            if (gt.bad) ok = false;  // PrunedAccess: the pair fails as GA_STUCK
+#endif
+            if (ok) book(P, L, w, d_min, o);
+            else finish(P, L, 3);
+        }
+    }
+    return r;
+}
+
 // One pass of the full tier's wavefront: lane q computes level d = d0+q of
 // full-width rows (distance.py:125-149, two 32-bit words); at step s it
 // evaluates column j = s - q + 1, taking R[d-1][j] from lane q-1 by shuffle
@@ -719,10 +865,19 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
 // hand-over list.  A separate instance, so the common case's code and
 // register allocation do not carry it (the shared instance measured 4 %
 // slower on config 3).
-template <bool kShare>
+template <bool kShare, bool kGroup>
 __global__ void __launch_bounds__(kTBlock, GA_THREAD_MINB)
 genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H) {
     const int lane = threadIdx.x & 31;
+    // kGroup: per warp, two group band tables and two mismatch rows (dynamic)
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* gtab = nullptr;
+    uint32_t* gpm = nullptr;
+    if (kGroup) {
+        uint32_t* wb = s_dyn + (threadIdx.x >> 5) * (2 * kGroupTabWords + 128);
+        gtab = wb + (lane >> 4) * kGroupTabWords;
+        gpm = wb + 2 * kGroupTabWords + (lane >> 4) * 64;
+    }
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t* region = band_base + gw * kBandWordsPerWarp;
     BandTab bt{reinterpret_cast<uint4*>(region), lane};
@@ -740,7 +895,8 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     L.pair = -1;
     for (;;) {
         // ---- free lanes take fresh pairs from the global longest-first queue ----
-        unsigned freem = __ballot_sync(FULL, L.pair < 0);
+        const bool want = L.pair < 0 && (!kGroup || (lane & (kGroupLanes - 1)) == 0);
+        unsigned freem = __ballot_sync(FULL, want);
         if (freem && !exhausted) {
             int cnt = __popc(freem);
             unsigned long long base = 0;
@@ -756,7 +912,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             base = __shfl_sync(FULL, base, 0);
             if (kShare && cnt == 0) capped = true;  // this SM's share is taken (the queue may not be)
             else if (base + cnt >= (unsigned long long)P.n_pairs) exhausted = true;
-            if (L.pair < 0 && (int)__popc(freem & lt) < cnt) {
+            if (want && (int)__popc(freem & lt) < cnt) {
                 const uint64_t idx = base + __popc(freem & lt);
                 if (idx < (uint64_t)P.n_pairs) {
                     fresh_pair(P, L, P.order ? P.order[idx] : (int)idx);
@@ -800,7 +956,8 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         const long long tw0 = clock64();
 #endif
         int r = WIN_NEXT;
-        if (L.pair >= 0) r = band_window(P, L, bt);
+        if (kGroup) r = group_window(P, L, gtab, gpm, lane);
+        else if (L.pair >= 0) r = band_window(P, L, bt);
         if (L.pair >= 0) {
             // a pair whose windows keep leaving the band tier (unrelated or very
             // divergent sequences) is handed over: the warps that run out of
@@ -829,6 +986,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         GA_STAT(5, clock64() - th0);
 #endif
 #ifndef GA_NO_DISCARD
+        if (!kGroup) {
         // the step's tables are dead once every lane has traced back: drop
         // their L2 lines without write-back, so they neither go to DRAM nor
         // crowd out the tables other warps are still reading
@@ -838,6 +996,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(region) + l * 128)
                          : "memory");
         __syncwarp();
+        }
 #endif
     }
 
@@ -923,8 +1082,8 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     if (base.W > 64) return cudaErrorInvalidValue;
     KernelParams P = base;
     int per_sm = 0;
-    cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, genasm_thread_kernel<false>, kTBlock, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, genasm_thread_kernel<false, false>, kTBlock, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const char* cap_env = getenv("GA_WARPS_PER_SM");
@@ -941,11 +1100,30 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     // %smid), and the warps without pairs serve the hand-over list
     // (genasm_thread_kernel<true>; config 4: 106 -> 83-91 ms).  Fewer in an
     // overlapped pipeline chunk: as many lanes as pairs.
-    const int sm_share = P.n_pairs < resident && !P.overlapped
+    // Pairs at most a quarter of the lanes: the lane-group kernel (two pairs
+    // per warp, 16 lanes each; genasm_thread_kernel<false, true>), whose
+    // window latency is what bounds such a batch.  GA_GROUP=0/1 forces it.
+    const size_t gsmem = (size_t)kWarps * (2 * kGroupTabWords + 128) * sizeof(uint32_t);
+    const char* genv = getenv("GA_GROUP");
+    const bool group = genv ? atoi(genv) != 0 : P.n_pairs * 4 <= resident;
+    int per_sm_g = per_sm;
+    if (group) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_g, genasm_thread_kernel<false, true>,
+                                                          kTBlock, gsmem);
+        if (e != cudaSuccess) return e;
+        if (per_sm_g < 1) return cudaErrorInvalidConfiguration;
+        if (bcap >= 1 && per_sm_g > bcap) per_sm_g = bcap;
+    }
+    const int sm_share = !group && P.n_pairs < resident && !P.overlapped
                              ? (int)((P.n_pairs + num_sms - 1) / num_sms) : 0;
     const int64_t lanes = P.n_pairs < resident ? P.n_pairs : resident;
-    const int grid = sm_share ? num_sms * per_sm : (int)((lanes + kTBlock - 1) / kTBlock > 0
-                                                         ? (lanes + kTBlock - 1) / kTBlock : 1);
+    int grid = sm_share ? num_sms * per_sm : (int)((lanes + kTBlock - 1) / kTBlock > 0
+                                                   ? (lanes + kTBlock - 1) / kTBlock : 1);
+    if (group) {
+        const int64_t gblocks = (P.n_pairs + 2 * kWarps - 1) / (2 * kWarps);
+        const int64_t gmax = (int64_t)num_sms * per_sm_g;
+        grid = (int)(gblocks < 1 ? 1 : (gblocks < gmax ? gblocks : gmax));
+    }
     // idle warps kept to serve hand-overs: only when this launch has the GPU
     // to itself (pipeline chunks overlap each other's launches, and a warp
     // lingering in one holds a slot the next needs: e2e 2.64 -> 2.07 M/s)
@@ -990,13 +1168,14 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     // the tracebacks write only the ops that are not '='
     if ((e = cudaMemsetAsync(P.ops, '=', (size_t)P.ops_capacity, stream))) return e;
     if ((e = cudaMemsetAsync(H.count, 0, 2 * sizeof(unsigned), stream))) return e;
-    if (sm_share) genasm_thread_kernel<true><<<grid, kTBlock, 0, stream>>>(P, band, H);
-    else genasm_thread_kernel<false><<<grid, kTBlock, 0, stream>>>(P, band, H);
+    if (group) genasm_thread_kernel<false, true><<<grid, kTBlock, gsmem, stream>>>(P, band, H);
+    else if (sm_share) genasm_thread_kernel<true, false><<<grid, kTBlock, 0, stream>>>(P, band, H);
+    else genasm_thread_kernel<false, false><<<grid, kTBlock, 0, stream>>>(P, band, H);
     shape->grid = grid;
     shape->block = kTBlock;
-    shape->smem_bytes = 0;
-    shape->group = 1;
-    shape->blocks_per_sm = per_sm;
+    shape->smem_bytes = group ? (int)gsmem : 0;
+    shape->group = group ? kGroupLanes : 1;
+    shape->blocks_per_sm = group ? per_sm_g : per_sm;
     shape->overflow_words_per_group = 0;
     shape->launches = 2;
     return cudaGetLastError();
