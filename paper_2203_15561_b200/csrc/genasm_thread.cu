@@ -31,7 +31,7 @@ namespace genasm {
 #ifdef GA_THREAD_STATS
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
-__device__ unsigned long long g_thread_stats[12];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB
+__device__ unsigned long long g_thread_stats[14];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB, [12] group window set-up
 // per pair: first window started, finished (globaltimer ns), full-tier windows
 __device__ unsigned long long g_pair_t[3][262144];
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
@@ -395,6 +395,129 @@ __device__ __forceinline__ uint32_t band_pm(const thr::Planes& pp, const thr::Pl
                         j - 1);
 }
 
+// Traceback of a group's window by its 16 lanes (backtrace.py:88-160), the
+// walk of coop_tb on the group's band table: lane q evaluates the state q
+// diagonal ('=') steps ahead; the first lane whose step is not '=' (ballot)
+// ends the run and its step is taken, so a run of up to 16 '=' and the edit
+// after it cost one round of shared-memory reads.  All 32 lanes run the
+// rounds (a group without a walk, or done, idles through them); counters are
+// group-uniform.  Returns false if the walk got stuck (or, GA_CHECK, read a
+// column below jlo: PrunedAccess).
+__device__ __forceinline__ bool group_tb(const uint32_t* gtab, bool walk, const thr::Planes& pp,
+                                         const thr::Planes& tp, int m, int n, int d_min, int budget,
+                                         int jlo, uint64_t prio_lut, uint8_t* ops, int64_t& nops,
+                                         thr::TbOut& o, int q, int lead) {
+    using namespace thr;
+    constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
+    const int o0 = m - n - 16;
+    bool bad = false;
+    auto word = [&](int e, int c) -> uint32_t {
+        if (!GA_ASSERT(c >= jlo && c <= n && e >= 0 && e < kFastLevels, 1, c, e)) {
+            bad = true;
+            return 0xffffffffu;
+        }
+        return gtab[(c - 1) * kFastLevels + e];
+    };
+    int d = d_min, j = n, i = m - 1;
+    o.consumed = o.tcons = o.wcost = 0;
+    o.reads = 0;
+    unsigned racc = 0;  // this lane's share of the entry reads
+    bool done = !walk, ok = true;
+#ifdef GA_THREAD_STATS
+    const int lane = q + lead;
+    int rounds = 0;
+#endif
+    for (;;) {
+        if (!done) {
+            if (i < 0 || o.consumed >= budget) {
+                done = true;
+            } else if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
+                if (i + 1 > d) {
+                    ok = false;
+                } else {
+                    const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
+                    for (int u = q; u < take; u += kGroupLanes) ops[nops + u] = 'I';
+                    nops += take;
+                    o.wcost += take;
+                    o.consumed += take;
+                }
+                done = true;
+            }
+        }
+        if (!__any_sync(FULL, !done)) break;
+#ifdef GA_THREAD_STATS
+        ++rounds;
+#endif
+        const int jq = j - q, iq = i - q;
+        int op = 4;  // this lane's state is past a limit (or the group is done): the run stops
+        unsigned rd = 0;
+        if (!done && iq >= 0 && o.consumed + q < budget && jq >= 1) {
+            const bool symeq = !bit64(tp.bn, jq - 1) && !bit64(pp.bn, iq) &&
+                               bit64(tp.b0, jq - 1) == bit64(pp.b0, iq) &&
+                               bit64(tp.b1, jq - 1) == bit64(pp.b1, iq);
+            const int dm1 = d > 0 ? d - 1 : 0;
+            const int u = i - (o0 + j);  // band position of (iq, jq): the same along the diagonal
+            uint32_t mb = 0, sb = 0, db, ib = 0;
+            if (jq == 1) {  // column 0 = init(m, .): bit x inactive iff x >= level
+                mb = iq - 1 >= d;
+                sb = iq - 1 >= d - 1;
+                db = iq >= d - 1;
+            } else {
+                const uint32_t w1 = word(dm1, jq - 1);
+                if (iq >= 1) {
+                    mb = (word(d, jq - 1) >> (u & 31)) & 1u;
+                    sb = (w1 >> (u & 31)) & 1u;
+                }
+                db = (w1 >> ((u + 1) & 31)) & 1u;
+            }
+            if (iq >= 1) ib = (word(dm1, jq) >> ((u - 1) & 31)) & 1u;
+            const bool dpos = d > 0;
+            const bool mok = symeq && (iq == 0 || !mb);
+            const bool sok = dpos && (iq == 0 || !sb);
+            const bool iok = dpos && (iq == 0 || !ib);
+            const bool dok = dpos && !db;
+            const unsigned okm =
+                (unsigned)mok | (unsigned)sok << 1 | (unsigned)iok << 2 | (unsigned)dok << 3;
+            op = (int)((prio_lut >> (4 * okm)) & 0xFu);
+            rd = (unsigned)(jq >= 2) + (dpos ? (unsigned)(jq >= 2) + 1u : 0u);
+        }
+        const unsigned nz = (__ballot_sync(FULL, op != OPC_M) >> lead) & 0xffffu;
+        const int f = nz ? __ffs(nz) - 1 : kGroupLanes;
+        const int opf = __shfl_sync(FULL, op, lead + (f & (kGroupLanes - 1)));
+        if (done) continue;
+        const bool taken = f < kGroupLanes && opf <= OPC_D;  // lane f's step is taken too
+        racc += (q < f || (taken && q == f)) ? rd : 0u;
+        j -= f;
+        i -= f;
+        o.consumed += f;
+        o.tcons += f;
+        nops += f;
+        if (f == kGroupLanes || opf == 4) continue;
+        if (opf > OPC_D) {
+            ok = false;
+            done = true;
+            continue;
+        }
+        if (q == 0) ops[nops] = (uint8_t)(kChars >> (8 * opf));
+        ++nops;
+        const int mj = opf != OPC_I, mi = opf != OPC_D;
+        j -= mj;
+        i -= mi;
+        d -= 1;
+        o.consumed += mi;
+        o.tcons += mj;
+        o.wcost += 1;
+    }
+#pragma unroll
+    for (int x = kGroupLanes / 2; x >= 1; x >>= 1) racc += __shfl_xor_sync(FULL, racc, x);
+    o.reads = racc;
+#ifdef GA_THREAD_STATS
+    GA_STAT(13, rounds);
+#endif
+    const bool any_bad = ((__ballot_sync(FULL, bad) >> lead) & 0xffffu) != 0;
+    return ok && !any_bad;
+}
+
 // One band-tier window per group (all 32 lanes call it; a group without a
 // pair idles through the shared steps).  The leader's return: WIN_HARD (state
 // untouched) if d_min > 15 and k allows more; otherwise the window is booked.
@@ -404,6 +527,9 @@ __device__ __forceinline__ int group_window(const KernelParams& P, Lane& L, uint
     const int q = lane & (kGroupLanes - 1);
     const int lead = lane & ~(kGroupLanes - 1);
     const int K = P.k;
+#ifdef GA_THREAD_STATS
+    const long long g0 = clock64();
+#endif
     Win w{};
     int run = 0;  // 1: the group computes a DC this step
     if (q == 0 && L.pair >= 0) {
@@ -442,6 +568,10 @@ __device__ __forceinline__ int group_window(const KernelParams& P, Lane& L, uint
     }
     const int jstore = band_jstore(n, budget);
     __syncwarp();  // mismatch words in; the previous window's table is no longer read
+#ifdef GA_THREAD_STATS
+    const long long g1 = clock64();
+    GA_STAT(12, g1 - g0);
+#endif
     // the wavefront: lane q holds level q
     const int o0 = m - n - 16;
     uint32_t c = init_band(m, q, o0);                     // R[q][j-1]
@@ -463,32 +593,50 @@ __device__ __forceinline__ int group_window(const KernelParams& P, Lane& L, uint
     __syncwarp();  // the table is complete
     // levels with R[d][n] bit m-1 (band bit 15) active
     const unsigned okv = __ballot_sync(FULL, run && !((c >> 15) & 1u));
+#ifdef GA_THREAD_STATS
+    const long long g2 = clock64();
+    GA_STAT(8, g2 - g1);
+#endif
+    uint32_t okm = (okv >> lead) & 0xffffu;
+    const int lim = K < 15 ? K : 15;
+    okm &= (2u << lim) - 1u;
     int r = WIN_NEXT;
-    if (q == 0 && run) {
-        uint32_t okm = (okv >> lead) & 0xffffu;
-        const int lim = K < 15 ? K : 15;
-        okm &= (2u << lim) - 1u;
-        if (!okm) {
-            if (K <= 15) finish(P, L, 1);
-            else r = WIN_HARD;
-        } else {
-            const int d_min = __ffs(okm) - 1;
-            GroupTab gt{gtab};
-#ifdef GA_CHECK
-            gt.jlo = jstore;
-            gt.jhi = n;
-            gt.bad = false;
-#endif
-            TbOut o;
-            bool ok = tb_band<false>(gt, pp, tp, m, n, d_min, budget, P.prio_lut, P.ops + L.ops,
-                                     L.nops, o);
-#ifdef GA_CHECK
-            if (gt.bad) ok = false;  // PrunedAccess: the pair fails as GA_STUCK
-#endif
-            if (ok) book(P, L, w, d_min, o);
-            else finish(P, L, 3);
-        }
+    if (q == 0 && run && !okm) {
+        if (K <= 15) finish(P, L, 1);
+        else r = WIN_HARD;
     }
+    // the walk, by the group's 16 lanes (group_tb); the leader books it
+    const bool walk = run && okm;
+    const int d_min = okm ? __ffs(okm) - 1 : 0;
+    int64_t nops = (int64_t)shfl64((uint64_t)L.nops, lead);
+    uint8_t* ops = P.ops + (int64_t)shfl64((uint64_t)L.ops, lead);
+    TbOut o;
+#ifdef GA_GROUP_SERIAL_TB
+    bool ok = true;
+    if (q == 0 && walk) {
+        GroupTab gt{gtab};
+#ifdef GA_CHECK
+        gt.jlo = jstore;
+        gt.jhi = n;
+        gt.bad = false;
+#endif
+        ok = tb_band<false>(gt, pp, tp, m, n, d_min, budget, P.prio_lut, ops, nops, o);
+#ifdef GA_CHECK
+        if (gt.bad) ok = false;
+#endif
+    }
+#else
+    const bool ok = group_tb(gtab, walk, pp, tp, m, n, d_min, budget, jstore, P.prio_lut, ops, nops, o,
+                             q, lead);
+#endif
+    if (q == 0 && walk) {
+        L.nops = nops;
+        if (ok) book(P, L, w, d_min, o);
+        else finish(P, L, 3);
+    }
+#ifdef GA_THREAD_STATS
+    GA_STAT(9, clock64() - g2);
+#endif
     return r;
 }
 
@@ -1195,9 +1343,9 @@ extern "C" void ga_debug_check(unsigned long long* out, int reset) {
 
 #ifdef GA_THREAD_STATS
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 12);
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 14);
     if (reset) {
-        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0};
+        unsigned long long z[14] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
         static unsigned long long pz[3][262144];
         for (int i = 0; i < 262144; ++i) pz[0][i] = ~0ull;
