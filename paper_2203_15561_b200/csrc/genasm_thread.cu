@@ -1162,7 +1162,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     // fresh-pair queue): hand-overs come only from warps before this point.
     // (A count of finished pairs instead -- one atomic per pair -- measured
     // 5 ms slower on config 3.)
-    if (kShare && lane == 0) atomicAdd(P.queue + 1, 1ull);
+    if ((kShare || kGroup) && lane == 0) atomicAdd(P.queue + 1, 1ull);
     bool lingering = false;
     unsigned nap = 250;
     // ---- handed-over pairs: a warp out of pairs claims the published ones,
@@ -1190,7 +1190,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             // unrelated or desynchronised pair whose every window needs the
             // full tier -- is taken at once instead of when its producer's
             // other pairs are done; the rest leave the SM.
-            if (!kShare) break;
+            if (!kShare && !kGroup) break;
             if (!lingering) {
                 int stay = 0;
                 if (lane == 0 && H.linger_cap)
@@ -1248,12 +1248,17 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     // %smid), and the warps without pairs serve the hand-over list
     // (genasm_thread_kernel<true>; config 4: 106 -> 83-91 ms).  Fewer in an
     // overlapped pipeline chunk: as many lanes as pairs.
-    // Pairs at most a quarter of the lanes: the lane-group kernel (two pairs
-    // per warp, 16 lanes each; genasm_thread_kernel<false, true>), whose
-    // window latency is what bounds such a batch.  GA_GROUP=0/1 forces it.
+    // Pairs at most an eighth of the lanes, the GPU to itself: the lane-group
+    // kernel (two pairs per warp, 16 lanes each; genasm_thread_kernel<false,
+    // true>), whose shorter window latency is what bounds such a batch.
+    // Measured (dev_kernel, ms): config 5 22.5 -> 9.4; config 3 first 8,000
+    // pairs 8.9 -> 8.6 but 17,366 pairs 10.5 -> 14.7 (two pairs per warp
+    // issue more per window than one lane each once the SMs fill up); e2e
+    // pipeline chunks keep the lane-per-pair kernel (2.08 -> 2.01 M/s with
+    // it).  GA_GROUP=0/1 forces the choice.
     const size_t gsmem = (size_t)kWarps * (2 * kGroupTabWords + 128) * sizeof(uint32_t);
     const char* genv = getenv("GA_GROUP");
-    const bool group = genv ? atoi(genv) != 0 : P.n_pairs * 4 <= resident;
+    const bool group = genv ? atoi(genv) != 0 : !P.overlapped && P.n_pairs * 8 <= resident;
     int per_sm_g = per_sm;
     if (group) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_g, genasm_thread_kernel<false, true>,
@@ -1268,15 +1273,17 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     int grid = sm_share ? num_sms * per_sm : (int)((lanes + kTBlock - 1) / kTBlock > 0
                                                    ? (lanes + kTBlock - 1) / kTBlock : 1);
     if (group) {
-        const int64_t gblocks = (P.n_pairs + 2 * kWarps - 1) / (2 * kWarps);
+        // a block per SM more than the pairs need, where it fits: its warps
+        // find no pair and stay to take hand-overs at once (the tail below)
+        const int64_t gblocks = (P.n_pairs + 2 * kWarps - 1) / (2 * kWarps) + num_sms;
         const int64_t gmax = (int64_t)num_sms * per_sm_g;
-        grid = (int)(gblocks < 1 ? 1 : (gblocks < gmax ? gblocks : gmax));
+        grid = (int)(gblocks < gmax ? gblocks : gmax);
     }
     // idle warps kept to serve hand-overs: only when this launch has the GPU
     // to itself (pipeline chunks overlap each other's launches, and a warp
     // lingering in one holds a slot the next needs: e2e 2.64 -> 2.07 M/s)
     const char* lc = getenv("GA_LINGER");
-    const int linger_cap = sm_share && !P.overlapped ? (lc ? atoi(lc) : 4) : 0;
+    const int linger_cap = (sm_share || group) && !P.overlapped ? (lc ? atoi(lc) : 4) : 0;
     // scratch: per-warp tables | bit-planes (one word per 64 symbols per
     // plane, plus a word of slack)
     const size_t warps = (size_t)grid * kWarps;
