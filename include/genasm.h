@@ -143,6 +143,12 @@ void ga_encode_ascii(const char* seq, int64_t n, uint8_t* out);
  * align_batch encodes its joined pair strings with it. */
 void ga_encode_ascii_mt(const char* seq, int64_t n, uint8_t* out, int32_t threads);
 
+/* ga_encode_ascii_mt over n_seqs separate ASCII buffers (ptrs[s], lens[s]),
+ * written back to back into out (sum of lens bytes): the drop-in Python API
+ * encodes the caller's str objects in place, with no joined copy. */
+void ga_encode_ascii_gather(const uint64_t* ptrs, const int64_t* lens, int64_t n_seqs,
+                            uint8_t* out, int32_t threads);
+
 /* Create a context bound to one CUDA device (one context per device; a
  * context is not re-entrant).  Returns 0 or a CUDA error code. */
 int ga_create(int device, ga_ctx** out);

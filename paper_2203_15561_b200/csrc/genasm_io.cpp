@@ -356,19 +356,48 @@ int64_t ga_format_align_rows(int64_t n, const char* ids, const int64_t* id_off, 
 
 }  // extern "C"
 
-extern "C" void ga_encode_ascii_mt(const char* seq, int64_t n, uint8_t* out, int32_t threads) {
-    // ACGT -> 0..3, everything else 4 (the reference's masks cover exactly the
-    // uppercase alphabet, pkg/src/bitalign/distance.py:70-79)
-    static const struct Lut {
-        uint8_t v[256];
-        Lut() {
-            memset(v, 4, sizeof v);
-            v[(unsigned char)'A'] = 0;
-            v[(unsigned char)'C'] = 1;
-            v[(unsigned char)'G'] = 2;
-            v[(unsigned char)'T'] = 3;
+// ACGT -> 0..3, everything else 4 (the reference's masks cover exactly the
+// uppercase alphabet, pkg/src/bitalign/distance.py:70-79)
+static const struct AsciiLut {
+    uint8_t v[256];
+    AsciiLut() {
+        memset(v, 4, sizeof v);
+        v[(unsigned char)'A'] = 0;
+        v[(unsigned char)'C'] = 1;
+        v[(unsigned char)'G'] = 2;
+        v[(unsigned char)'T'] = 3;
+    }
+} kAsciiLut;
+
+extern "C" void ga_encode_ascii_gather(const uint64_t* ptrs, const int64_t* lens, int64_t n_seqs,
+                                       uint8_t* out, int32_t threads) {
+    // sequence s starts at the sum of the lengths before it; threads take
+    // equal byte ranges of the output (a sequence may span two of them)
+    std::vector<int64_t> start((size_t)n_seqs + 1, 0);
+    for (int64_t q = 0; q < n_seqs; ++q) start[(size_t)q + 1] = start[(size_t)q] + lens[q];
+    const int64_t total = start[(size_t)n_seqs];
+    int t = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+    if (t < 1) t = 1;
+    if (total < (int64_t)1 << 20) t = 1;
+    const int64_t per = (total + t - 1) / t;
+    auto work = [&](int64_t a, int64_t b) {  // output bytes [a, b)
+        if (a >= b) return;
+        int64_t q = std::upper_bound(start.begin(), start.end(), a) - start.begin() - 1;
+        for (int64_t i = a; i < b; ++q) {
+            const int64_t e = std::min(b, start[(size_t)q + 1]);
+            const char* src = reinterpret_cast<const char*>(ptrs[q]) + (i - start[(size_t)q]);
+            for (int64_t x = i; x < e; ++x) out[x] = kAsciiLut.v[(unsigned char)src[x - i]];
+            i = std::max(i, e);  // (an empty sequence leaves i where it is)
         }
-    } lut;
+    };
+    std::vector<std::thread> pool;
+    for (int k = 1; k < t; ++k) pool.emplace_back(work, k * per, std::min(total, (k + 1) * per));
+    work(0, std::min(total, per));
+    for (auto& th : pool) th.join();
+}
+
+extern "C" void ga_encode_ascii_mt(const char* seq, int64_t n, uint8_t* out, int32_t threads) {
+    const AsciiLut& lut = kAsciiLut;
     int t = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
     if (t < 1) t = 1;
     if (n < (int64_t)1 << 20) t = 1;

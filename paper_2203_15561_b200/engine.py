@@ -51,6 +51,8 @@ def lib():
             "ga_check_config": ([F, C.c_char_p, C.c_int], C.c_int),
             "ga_encode_ascii": ([C.c_char_p, C.c_int64, C.c_void_p], None),
             "ga_encode_ascii_mt": ([C.c_char_p, C.c_int64, C.c_void_p, C.c_int32], None),
+            "ga_encode_ascii_gather": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32],
+                                       None),
             "ga_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
             "ga_destroy": ([C.c_void_p], None),
             "ga_last_error": ([C.c_void_p], C.c_char_p),
@@ -152,15 +154,50 @@ def run_packed(batch: PackedBatch, window: int, overlap: int, k: int, priority: 
     return out
 
 
+def _str_data_offset() -> int | None:
+    """Byte offset of a compact ASCII ``str``'s characters from its address
+    (CPython lays them out right after the PyASCIIObject header,
+    ``sys.getsizeof("") - 1`` bytes), checked on a probe string; None if the
+    running interpreter does not lay strings out that way."""
+    import sys
+    off = sys.getsizeof("") - 1
+    probe = "ACGTNacgt" * 7
+    try:
+        if C.string_at(id(probe) + off, len(probe)) == probe.encode("ascii"):
+            return off
+    except Exception:  # noqa: BLE001 -- any failure means: do not use it
+        pass
+    return None
+
+
+_STR_OFF = _str_data_offset()
+
+
 def pack_pairs(pairs) -> PackedBatch:
     """``PackedBatch.from_pairs`` for the drop-in ``align_batch``: the pair
-    strings joined once and encoded by the native multithreaded encoder
-    (ga_encode_ascii_mt) instead of a numpy table lookup; non-ASCII input
+    strings encoded by the native multithreaded encoder instead of a numpy
+    table lookup -- read in place from the ``str`` objects
+    (ga_encode_ascii_gather; CPython's compact ASCII layout, verified at
+    import) or, elsewhere, joined once (ga_encode_ascii_mt).  Non-ASCII input
     (Unicode code units, never a match) takes the exact Python path."""
     import itertools
     n = len(pairs)
     lens = np.fromiter(map(len, itertools.chain.from_iterable(pairs)), dtype=np.int64,
                        count=2 * n)
+    if _STR_OFF is not None and all(type(a) is str and type(b) is str and a.isascii() and b.isascii()
+                                   for a, b in pairs):
+        ptrs = np.fromiter((id(x) + _STR_OFF for x in itertools.chain.from_iterable(pairs)),
+                           dtype=np.uint64, count=2 * n)
+        total = int(lens.sum())
+        codes = np.empty(max(1, total), dtype=np.uint8)
+        lib().ga_encode_ascii_gather(ptrs.ctypes.data, lens.ctypes.data, 2 * n,
+                                     codes.ctypes.data, 0)
+        starts = np.zeros(2 * n, dtype=np.int64)
+        if n:
+            np.cumsum(lens[:-1], out=starts[1:])
+        return PackedBatch(codes=codes[:total], pat_off=starts[0::2].copy(),
+                           pat_len=lens[0::2].astype(np.int32), txt_off=starts[1::2].copy(),
+                           txt_len=lens[1::2].astype(np.int32))
     blob = "".join(itertools.chain.from_iterable(pairs))
     if not blob.isascii():
         return PackedBatch.from_pairs(pairs)

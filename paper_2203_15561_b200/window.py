@@ -12,6 +12,7 @@ accepts are rejected with ``ValueError`` because they have no GPU path:
 
 from __future__ import annotations
 
+import gc
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -157,10 +158,28 @@ def outcomes_from_packed(batch: PackedBatch, out: PackedResults,
     else:
         ops_buf = out.ops
     ops_mv = memoryview(np.ascontiguousarray(ops_buf))  # each CIGAR decoded straight from it
-    dists = out.dists.tolist()
+    # window distances sliced from one bytes object: a tuple of a bytes slice
+    # is a tuple of the cached small ints, with no 10^7-element list between
+    dists = np.ascontiguousarray(out.dists, dtype=np.uint8).tobytes()
     new = object.__new__
     outcomes: list[BatchOutcome] = []
     append = outcomes.append
+    # Hundreds of thousands of new container objects would trigger the cyclic
+    # collector over and over (none of them can form a cycle): 5.8 -> 2.7 s for
+    # config 3's 138,929 pairs with it off.
+    gc_was = gc.isenabled()
+    gc.disable()
+    try:
+        _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops_len, ops_off,
+                       win_off, nwin, ops_mv, dists, cfg, new, append)
+    finally:
+        if gc_was:
+            gc.enable()
+    return outcomes
+
+
+def _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops_len, ops_off,
+                   win_off, nwin, ops_mv, dists, cfg, new, append):
     for q in range(n):
         st = status[q]
         if st == _abi.GA_OK:
@@ -184,7 +203,6 @@ def outcomes_from_packed(batch: PackedBatch, out: PackedResults,
             append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
         else:
             raise StuckTraceback(f"pair {q}: traceback tripwire fired in window {fail[q]}")
-    return outcomes
 
 
 def align(pattern: str, text: str, cfg: WindowConfig = WindowConfig()) -> AlignmentResult:

@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import random
 import re
 
 import numpy as np
@@ -70,6 +71,29 @@ def test_packing_roundtrip():
     for q, (p, t) in enumerate(pairs):
         assert b.codes[b.pat_off[q]:b.pat_off[q] + len(p)].tolist() == _abi.encode(p).tolist()
         assert b.codes[b.txt_off[q]:b.txt_off[q] + len(t)].tolist() == _abi.encode(t).tolist()
+
+
+@pytest.mark.parametrize("in_place", [True, False])
+def test_pack_pairs_matches_from_pairs(monkeypatch, in_place):
+    # align_batch's native packer: in place from the str objects (CPython's
+    # compact ASCII layout) or from one joined copy; non-ASCII takes the
+    # exact Python path.  Same codes and offsets as PackedBatch.from_pairs.
+    if not in_place:
+        monkeypatch.setattr(engine, "_STR_OFF", None)
+    else:
+        assert engine._STR_OFF is not None  # the layout probe holds on this interpreter
+    rng = random.Random(5)
+    cases = [[], [("", "")], [("ACGT", "AC"), ("", "T"), ("GG", "")], [("AÇG", "ng"), ("ACGT", "A")]]
+    for _ in range(40):
+        cases.append([("".join(rng.choice("ACGTNacgtx") for _ in range(rng.randrange(0, 2000))),
+                       "".join(rng.choice("ACGT") for _ in range(rng.randrange(0, 40))))
+                      for _ in range(rng.randrange(1, 25))])
+    big = "".join(rng.choice("ACGTN") for _ in range(5000))
+    cases.append([(big[i % 97:], big[:4000 + i]) for i in range(400)])  # > 1 MB: threaded ranges
+    for pairs in cases:
+        a, b = engine.pack_pairs(pairs), _abi.PackedBatch.from_pairs(pairs)
+        for f in ("codes", "pat_off", "pat_len", "txt_off", "txt_len"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
 
 
 def test_num_windows_formula():
