@@ -197,9 +197,6 @@ __device__ __noinline__ void fail_pair(PairResult* results, uint8_t* dists, int 
 // correct.  The by-reference form measured 1.5 % faster on config 3; it is not
 // worth a code-shape-dependent miscompile (DESIGN 9).
 __device__ __forceinline__ void finish(const KernelParams& P, Lane& L, int status) {
-#ifdef GA_DEV_FINISH_ATOMIC
-    atomicAdd_system(&g_finished, 1ull);
-#endif
     if (status == 0) {
         PairResult r;
         r.status = 0;
@@ -751,9 +748,9 @@ struct HandList {
     int32_t* list;      // pair ids by ticket, -1 until published
     unsigned* count;    // tickets handed out to producers
     unsigned* claim;    // tickets taken by consumers
-    unsigned* finished; // pairs finished (any status)
     unsigned* sm_claims;  // per SM (by %smid): fresh pairs taken / warps lingering
     unsigned* linger;
+    unsigned* started;  // blocks of this launch that have started
     int sm_share;       // fresh pairs per SM when pairs are fewer than lanes (else 0)
     int linger_cap;     // warps per SM that stay to serve hand-overs (else 0)
 };
@@ -1026,6 +1023,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         gtab = wb + (lane >> 4) * kGroupTabWords;
         gpm = wb + 2 * kGroupTabWords + (lane >> 4) * 64;
     }
+    if ((kShare || kGroup) && threadIdx.x == 0) atomicAdd(H.started, 1u);
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t* region = band_base + gw * kBandWordsPerWarp;
     BandTab bt{reinterpret_cast<uint4*>(region), lane};
@@ -1192,8 +1190,13 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             // other pairs are done; the rest leave the SM.
             if (!kShare && !kGroup) break;
             if (!lingering) {
+                // Only while every block of the launch has started: a warp
+                // that waited for hand-overs while blocks of its own grid
+                // could not be scheduled (another launch holding part of the
+                // GPU) could wait for warps that never run.
                 int stay = 0;
-                if (lane == 0 && H.linger_cap)
+                if (lane == 0 && H.linger_cap &&
+                    *(volatile unsigned*)H.started >= gridDim.x)
                     stay = (int)atomicAdd(H.linger + smid(), 1u) < H.linger_cap;
                 if (!__shfl_sync(FULL, stay, 0)) break;
                 lingering = true;
@@ -1291,7 +1294,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     const int64_t pw = (P.codes_len + 63) / 64 + 1;
     const size_t plane_total = ((size_t)pw * 3 * 2 + 63) & ~(size_t)63;
     const size_t list_words = ((size_t)P.n_pairs + 63 + 64) & ~(size_t)63;
-    const size_t need = band_words + plane_total + list_words + 2 * kSmSlots;
+    const size_t need = band_words + plane_total + list_words + 2 * kSmSlots + 32;
     if (need > *cap || !*scratch) {
         if (*scratch) cudaFree(*scratch);
         *scratch = nullptr;
@@ -1316,9 +1319,10 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     H.claim = H.count + 1;
     H.sm_claims = *scratch + band_words + plane_total + list_words;
     H.linger = H.sm_claims + kSmSlots;
+    H.started = H.linger + kSmSlots;
     H.sm_share = sm_share;
     H.linger_cap = linger_cap;
-    if ((e = cudaMemsetAsync(H.sm_claims, 0, 2 * kSmSlots * 4, stream))) return e;
+    if ((e = cudaMemsetAsync(H.sm_claims, 0, (2 * kSmSlots + 32) * 4, stream))) return e;
     if ((e = cudaMemsetAsync(H.list, 0xff, (size_t)P.n_pairs * 4, stream))) return e;
     // the tracebacks write only the ops that are not '='
     if ((e = cudaMemsetAsync(P.ops, '=', (size_t)P.ops_capacity, stream))) return e;
