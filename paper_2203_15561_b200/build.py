@@ -56,5 +56,29 @@ def build(force: bool = False, verbose: bool = False, check: bool = False) -> st
     return so
 
 
+def outcomes_so() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_outcomes" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_outcomes(force: bool = False) -> str:
+    """The CPython extension that builds the drop-in API's result objects in
+    bulk (csrc/outcomes_py.cpp; host code, g++ against this interpreter)."""
+    import sysconfig
+    so = outcomes_so()
+    src = os.path.join(CSRC, "outcomes_py.cpp")
+    if not force and os.path.exists(so) and os.path.getmtime(so) >= os.path.getmtime(src):
+        return so
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC",
+           "-I" + sysconfig.get_paths()["include"], "-o", so + ".tmp", src]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stdout + proc.stderr)
+        raise RuntimeError("g++ failed building _outcomes")
+    os.replace(so + ".tmp", so)
+    return so
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True, check="--check" in sys.argv)
+    build_outcomes(force="--force" in sys.argv)

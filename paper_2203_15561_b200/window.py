@@ -20,6 +20,11 @@ import numpy as np
 from . import _abi
 from ._abi import PackedBatch, PackedResults
 
+try:  # bulk construction of the result objects (csrc/outcomes_py.cpp, build.py)
+    from . import _outcomes
+except ImportError:  # not built: the same objects from the Python loop
+    _outcomes = None
+
 DEFAULT_WINDOW = 64
 DEFAULT_OVERLAP = 24
 DEFAULT_PRIORITY = "MSID"
@@ -170,12 +175,39 @@ def outcomes_from_packed(batch: PackedBatch, out: PackedResults,
     gc_was = gc.isenabled()
     gc.disable()
     try:
-        _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops_len, ops_off,
-                       win_off, nwin, ops_mv, dists, cfg, new, append)
+        if _outcomes is not None:
+            # the aligned pairs' objects in one native call (csrc/outcomes_py.cpp)
+            ops_arr = np.ascontiguousarray(ops_buf)
+            dist_arr = np.ascontiguousarray(out.dists, dtype=np.uint8)
+            cols = [np.ascontiguousarray(res[f], dtype=np.int64) for f in
+                    ("cost", "text_consumed", "rows_computed", "entry_reads", "entry_writes",
+                     "words_allocated", "ops_len")]
+            st = np.ascontiguousarray(res["status"], dtype=np.int32)
+            offs = [np.ascontiguousarray(x, dtype=np.int64) for x in
+                    (out.ops_off, out.win_off, np.asarray(nwin, dtype=np.int64))]
+            outcomes = _outcomes.build(AlignmentResult, AccessCounters, BatchOutcome, n,
+                                       st.ctypes.data, *(c.ctypes.data for c in cols),
+                                       *(o.ctypes.data for o in offs), ops_arr.ctypes.data,
+                                       dist_arr.ctypes.data)
+            for q in np.flatnonzero(st != _abi.GA_OK).tolist():
+                outcomes[q] = _failed_outcome(status[q], fail[q], q, cfg)
+        else:
+            _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops_len,
+                           ops_off, win_off, nwin, ops_mv, dists, cfg, new, append)
     finally:
         if gc_was:
             gc.enable()
     return outcomes
+
+
+def _failed_outcome(st: int, fail_window: int, q: int, cfg: WindowConfig) -> BatchOutcome:
+    if st == _abi.GA_WINDOW_FAILED:
+        exc = WindowFailed(fail_window, cfg.k)
+        return BatchOutcome(error=f"{type(exc).__name__}: {exc}")
+    if st == _abi.GA_EMPTY_PATTERN:
+        exc = EmptyPattern("pattern must not be empty")
+        return BatchOutcome(error=f"{type(exc).__name__}: {exc}")
+    raise StuckTraceback(f"pair {q}: traceback tripwire fired in window {fail_window}")
 
 
 def _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops_len, ops_off,
@@ -195,14 +227,8 @@ def _fill_outcomes(n, status, cost, tcons, rows, reads, writes, words, fail, ops
             b = new(BatchOutcome)
             b.__dict__.update(result=r, error=None)
             append(b)
-        elif st == _abi.GA_WINDOW_FAILED:
-            exc = WindowFailed(fail[q], cfg.k)
-            append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
-        elif st == _abi.GA_EMPTY_PATTERN:
-            exc = EmptyPattern("pattern must not be empty")
-            append(BatchOutcome(error=f"{type(exc).__name__}: {exc}"))
         else:
-            raise StuckTraceback(f"pair {q}: traceback tripwire fired in window {fail[q]}")
+            append(_failed_outcome(st, fail[q], q, cfg))
 
 
 def align(pattern: str, text: str, cfg: WindowConfig = WindowConfig()) -> AlignmentResult:

@@ -116,6 +116,39 @@ def test_outcomes_from_packed_shapes():
     assert outs[2].error == "EmptyPattern: pattern must not be empty"
 
 
+def test_outcomes_native_builder_matches_python_loop(monkeypatch):
+    # csrc/outcomes_py.cpp builds the same objects as the Python loop:
+    # equal outcomes, the dataclass's field order in every result's __dict__
+    from paper_2203_15561_b200 import window
+    if window._outcomes is None:
+        pytest.skip("_outcomes not built (build.py builds it)")
+    rng = np.random.default_rng(1)
+    prng = random.Random(2)
+    pairs = [("".join(prng.choice("ACGT") for _ in range(prng.randrange(0, 900))),
+              "ACGT" * prng.randrange(0, 50)) for _ in range(300)]
+    b = _abi.PackedBatch.from_pairs(pairs)
+    out = _abi.PackedResults.allocate(b, 64, 24)
+    n, res = b.n_pairs, out.results
+    res["status"] = rng.choice([0, 0, 0, 1, 2], n)
+    for f in ("cost", "text_consumed", "rows_computed", "entry_reads", "entry_writes",
+              "words_allocated"):
+        res[f] = rng.integers(0, 10**9, n)
+    res["fail_window"] = rng.integers(0, 5, n)
+    cap = np.diff(np.append(out.ops_off, out.ops.shape[0]))
+    res["ops_len"] = [rng.integers(0, c + 1) for c in cap]
+    out.ops[:] = rng.choice(np.frombuffer(b"=XID", np.uint8), out.ops.shape[0])
+    out.dists[:] = rng.integers(0, 64, out.dists.shape[0])
+    cfg = ga.WindowConfig(window=64, overlap=24, k=64)
+    native = window.outcomes_from_packed(b, out, cfg)
+    monkeypatch.setattr(window, "_outcomes", None)
+    loop = window.outcomes_from_packed(b, out, cfg)
+    assert native == loop and sum(x.ok for x in native) > 100
+    for x, y in zip(native, loop):
+        if x.ok:
+            assert list(vars(x.result)) == list(vars(y.result))
+            assert vars(x.result.counters) == vars(y.result.counters)
+
+
 def test_lpt_split_balances_and_partitions():
     rng = np.random.default_rng(0)
     lens = rng.integers(100, 50_000, size=1000).astype(np.int32)
