@@ -1258,9 +1258,9 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     // pairs 8.9 -> 8.6 but 17,366 pairs 10.5 -> 14.7 (two pairs per warp
     // issue more per window than one lane each once the SMs fill up); e2e
     // pipeline chunks keep the lane-per-pair kernel (2.08 -> 2.01 M/s with
-    // it).  GA_GROUP=0/1 forces the choice.
+    // it).  GA_LANE_GROUPS=0/1 forces the choice.
     const size_t gsmem = (size_t)kWarps * (2 * kGroupTabWords + 128) * sizeof(uint32_t);
-    const char* genv = getenv("GA_GROUP");
+    const char* genv = getenv("GA_LANE_GROUPS");
     const bool group = genv ? atoi(genv) != 0 : !P.overlapped && P.n_pairs * 8 <= resident;
     int per_sm_g = per_sm;
     if (group) {

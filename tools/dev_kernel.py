@@ -2,7 +2,8 @@
 
     python tools/dev_kernel.py [config] [count] [reps]
 Runs ga_align_batch_device `reps` times on one config's pairs (inputs already
-in HBM) and prints the CUDA-event time per launch.  Knobs: GA_GROUP,
+in HBM) and prints the CUDA-event time per launch (W = GA_DEV_W, default 64,
+O = 3W/8 or 24 at 64, k = GA_DEV_K, default W).  Knobs: GA_LANE_GROUPS (0/1: the 16-lane group kernel), GA_GROUP (lockstep group size),
 GA_BLOCK, GA_WARPS_PER_SM (read by the library at each launch).
 """
 
@@ -27,9 +28,11 @@ def main():
     n = batch.n_pairs
     L = engine.lib()
     ctx = engine.context(0)
-    cfg = _abi.make_config(64, 24, int(os.environ.get("GA_DEV_K", 64)), "MSID",
+    W = int(os.environ.get("GA_DEV_W", 64))
+    O = 3 * W // 8 if W != 64 else 24
+    cfg = _abi.make_config(W, O, int(os.environ.get("GA_DEV_K", W)), "MSID",
                            os.environ.get("GA_MODE", "improved"))
-    host = _abi.PackedResults.allocate(batch, 64, 24)
+    host = _abi.PackedResults.allocate(batch, W, O)
     dev = torch.device("cuda:0")
     up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     order = engine.lpt_order(batch.pat_len)
