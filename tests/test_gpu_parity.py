@@ -291,6 +291,21 @@ def test_config3_full_vs_oracle(gpu, oracle_mod):
     assert (got.results["status"] == 0).all()  # k = W: every window aligns
 
 
+def test_config3_shard_on_lane_groups(gpu, oracle_mod, monkeypatch):
+    """An 8-GPU shard of config 3 (17,367 pairs) forced onto the 16-lane group
+    kernel (two waves of groups, hard windows, the lingering warps), every
+    field and every op byte against the oracle."""
+    from paper_2203_15561_b200 import sim
+    from paper_2203_15561_b200.engine import run_packed
+    monkeypatch.setenv("GA_LANE_GROUPS", "1")
+    batch, _ = sim.config_pairs(3, count=17_367)
+    got = run_packed(batch, 64, 24, 64, "MSID")
+    exp = oracle_mod.align_packed(batch, 64, 24, 64, "MSID", threads=os.cpu_count())
+    assert np.array_equal(got.results, exp.results)
+    assert np.array_equal(got.dists, exp.dists)
+    assert _all_ops_equal(got, exp, "config3 shard, lane groups") > 100_000_000
+
+
 def test_config4_full_vs_oracle(gpu, oracle_mod):
     """All 20,000 ultra-long config-4 pairs (~2,450-window chains, the
     reference's window loop pkg/src/bitalign/window.py:95-120), every field and
@@ -346,13 +361,18 @@ def test_full_tier_beyond_level_63(gpu, oracle_mod):
         _packed_equal(got, exp, ("deep", prio))
 
 
-@pytest.mark.parametrize("kernel", ["thread", "lockstep"])
+@pytest.mark.parametrize("kernel", ["thread", "lanegroups", "lockstep"])
 def test_both_kernels_vs_oracle(gpu, oracle_mod, monkeypatch, kernel):
-    """Each kernel on its own (GA_KERNEL): the lane-per-pair kernel with its
-    band / full tiers and hand-over, and the lane-group kernel."""
+    """Each kernel on its own, whatever the batch size would pick: the
+    lane-per-pair kernel with its band / full tiers and hand-over
+    (GA_LANE_GROUPS=0), the 16-lane group kernel (GA_LANE_GROUPS=1) and the
+    lockstep kernel (GA_KERNEL=lockstep)."""
     from paper_2203_15561_b200 import sim
     from paper_2203_15561_b200.engine import run_packed
-    monkeypatch.setenv("GA_KERNEL", kernel)
+    if kernel == "lockstep":
+        monkeypatch.setenv("GA_KERNEL", "lockstep")
+    else:
+        monkeypatch.setenv("GA_LANE_GROUPS", "1" if kernel == "lanegroups" else "0")
     batch, _ = sim.config_pairs(5)
     for (w, o, k, prio) in [(64, 24, 64, "MSID"), (64, 24, 16, "DISM"), (32, 12, 32, "SMDI"),
                             (48, 18, 30, "IDSM")]:
