@@ -1,4 +1,5 @@
-// genasm_thread.cu -- lane-per-pair fused DC+TB kernel (sm_100a), W <= 64.
+// genasm_thread.cu -- lane-per-pair fused DC+TB kernel (sm_100a), W <= 64,
+// and its 16-lane-group form for small batches (the latency path, below).
 //
 // Every lane owns one pair and walks its window chain (window.py:95-120)
 // alone: DC in 32-bit diagonal bands (16 levels, exact for d_min <= 15; see
@@ -11,7 +12,7 @@
 // owns level q (0..31) of full-width rows and the 32 lanes sweep the window
 // as a wavefront (n + 31 steps, one shuffle of R[q-1][j] per step), storing
 // the rows in the warp's table (further passes of 32 levels as k allows, lane
-// 0 reading the row lane 31 stored); the owner lane then traces back alone.
+// 0 reading the row lane 31 stored); the warp traces back together (coop_tb).
 //
 // Fresh pairs come from a global longest-first queue, the grid fills every SM
 // equally.  A pair with 4 consecutive windows beyond the band tier is handed
@@ -344,15 +345,15 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
 }
 
 // ---- lane groups: the latency path for batches far smaller than the
-// resident lanes (genasm_thread_kernel<false, true>).  Each half-warp owns one
-// pair; lane q of the group computes band level q (0..15) of every column as
-// a wavefront -- at step s it evaluates column j = s - q + 1, R[q-1][j] from
-// lane q-1 by shuffle -- so a window's DC takes n + 15 steps of one level
-// each instead of n columns of 16 levels on one lane.  The window's band
-// table is in shared memory, [column][level] unrotated (the band tier's
-// exactness argument needs no rotation; rotating levels 8..15 only served the
-// pairing of dc_band), and the group's leader (lane 0 / 16) traces back from
-// it alone with tb_band. ----
+// resident lanes (genasm_thread_kernel<false, true>; DESIGN 3).  Each
+// half-warp owns one pair; lane q of the group computes band level q (0..15)
+// of every column as a wavefront -- at step s it evaluates column
+// j = s - q + 1, R[q-1][j] from lane q-1 by shuffle -- so a window's DC takes
+// n + 15 steps of one level each instead of n columns of 16 levels on one
+// lane.  The window's band table is in shared memory, [column][level]
+// unrotated (the band tier's exactness argument needs no rotation; rotating
+// levels 8..15 only served the pairing of dc_band), and the group's 16 lanes
+// trace back from it together (group_tb). ----
 constexpr int kGroupLanes = 16;
 constexpr int kGroupTabWords = 64 * thr::kFastLevels + 16;  // + 16: the two groups' banks differ
 
@@ -1249,7 +1250,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     // the queue.  Fewer, with the GPU to itself (the device call, a one-chunk
     // host call): still every warp, an equal share of the pairs per SM (by
     // %smid), and the warps without pairs serve the hand-over list
-    // (genasm_thread_kernel<true>; config 4: 106 -> 83-91 ms).  Fewer in an
+    // (genasm_thread_kernel<true, false>; config 4: 106 -> 83-91 ms).  Fewer in an
     // overlapped pipeline chunk: as many lanes as pairs.
     // Pairs at most an eighth of the lanes, the GPU to itself: the lane-group
     // kernel (two pairs per warp, 16 lanes each; genasm_thread_kernel<false,
