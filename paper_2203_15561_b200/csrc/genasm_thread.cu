@@ -642,45 +642,37 @@ __device__ __forceinline__ int group_window(const KernelParams& P, Lane& L, uint
 // full-width rows (distance.py:125-149, two 32-bit words); at step s it
 // evaluates column j = s - q + 1, taking R[d-1][j] from lane q-1 by shuffle
 // (lane q-1 produced it the step before).  Lane 0 of a later pass (kCarry)
-// reads R[d0-1][j] -- stored by lane 31 in the pass before -- from the table,
-// a few steps ahead; the first pass has no carry and holds level 0.  Rows go
-// to out[s * 32] (step-major, full_index).  The steps are branch-free: a lane
-// outside 1 <= j <= n computes and discards.  Measured on the warp's own
-// (tools/coop_bench.cu, cycles per 95-step pass, one warp per SM partition):
-// a carry load in the first pass's steps, even predicated off, 11.5 k against
-// 6-8 k without; the carry through shared memory instead (lane 31 stores,
-// lane 0 loads) 13.4-13.9 k; the next step's mismatch words loaded a step
-// ahead 9.5 k against 8.0 k.
+// reads R[d0-1][j] -- lane 31's rows of the pass before, which coop_dc copies
+// to shared memory between the passes; the first pass has no carry and holds
+// level 0.  Rows go to out[s * 32] (step-major, full_index).  The steps are
+// branch-free: a lane outside 1 <= j <= n computes and discards.  Measured on
+// the warp's own (tools/coop_bench.cu, cycles per 95-step pass, one warp per
+// SM partition): a carry load in the first pass's steps, even predicated off,
+// 11.5 k against 6-8 k without; the carry stored and loaded through shared
+// memory inside the steps (lane 31 stores, lane 0 loads) 13.4-13.9 k; the
+// next step's mismatch words loaded a step ahead 9.5 k against 8.0 k.
 template <bool kCarry>
 __device__ __forceinline__ void coop_pass(int m, int n, int d, uint64_t* out, const uint2* pmt,
                                           int q, uint32_t& cl, uint32_t& ch) {
     using namespace thr;
-    constexpr int kAhead = 4;  // carry rows in flight
     const uint64_t a0 = d > 0 ? init_row64(m, d - 1) : 0ull;  // R[d-1][0]
     uint32_t al = (uint32_t)a0, ah = (uint32_t)(a0 >> 32);
     uint32_t ol = 0, oh = 0;  // this lane's last output
     const bool lvl0 = !kCarry && q == 0;
     const bool keep = d <= m;  // d_min <= m: no level above m is ever read
     const int S = n + kFullLevels - 1;
-    // lane 0 of a later pass: R[d0-1][s+1], stored by lane 31 of the pass
-    // before at its step s+31, i.e. at cin[s * 32]
-    const uint64_t* cin = out - 96 * kFullLevels + (kFullLevels - 1) * kFullLevels + (kFullLevels - 1);
-    uint64_t cv[kAhead];
-    if (kCarry) {
-#pragma unroll
-        for (int u = 0; u < kAhead; ++u) cv[u] = q == 0 && u < n ? cin[u * kFullLevels] : 0ull;
-    }
+    // lane 0 of a later pass: R[d0-1][s+1] from the carry row coop_dc copied
+    // to pmt[64 + s], read a step ahead
+    uint2 cv = kCarry ? pmt[64] : make_uint2(0u, 0u);
 #pragma unroll 2
     for (int s = 0; s < S; ++s) {
         uint32_t bl = __shfl_up_sync(FULL, ol, 1), bh = __shfl_up_sync(FULL, oh, 1);
         const int j = s - q + 1;
         const bool valid = (unsigned)(j - 1) < (unsigned)n;
         if (kCarry) {
-            bl = q == 0 ? (uint32_t)cv[0] : bl;
-            bh = q == 0 ? (uint32_t)(cv[0] >> 32) : bh;
-#pragma unroll
-            for (int u = 0; u + 1 < kAhead; ++u) cv[u] = cv[u + 1];
-            cv[kAhead - 1] = q == 0 && s + kAhead < n ? cin[(size_t)(s + kAhead) * kFullLevels] : 0ull;
+            bl = q == 0 ? cv.x : bl;
+            bh = q == 0 ? cv.y : bh;
+            cv = pmt[64 + (s + 1 < n ? s + 1 : 0)];
         }
         const uint2 pm = pmt[valid ? j - 1 : 0];
         const uint32_t xl = cl << 1, xh = shl1_hi(cl, ch);
@@ -705,8 +697,8 @@ __device__ __forceinline__ void coop_pass(int m, int n, int d, uint64_t* out, co
 
 // Full tier, the whole warp on one window: passes of 32 levels (coop_pass),
 // rows stored to tab[full_index(d, j)], until a level <= k has R[d][n] bit
-// m-1 active or the passes cover kmax.  Returns that d_min, or -1.  pmt: the
-// window's mismatch words (64, shared memory).
+// m-1 active or the passes cover kmax.  Returns that d_min, or -1.  pmt: 128
+// words of shared memory, the window's mismatch words and the carry row.
 __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes& tp, int m, int n,
                                        int K, int kmax, uint64_t* tab, uint2* pmt, int lane) {
     using namespace thr;
@@ -739,6 +731,18 @@ __device__ __forceinline__ int coop_dc(const thr::Planes& pp, const thr::Planes&
         const bool hit = d <= K && d <= m && !(((uint64_t)ch << 32 | cl) >> (m - 1) & 1ull);
         const unsigned hm = __ballot_sync(FULL, hit);
         if (hm) return d0 + __ffs(hm) - 1;
+        // another pass: its lane 0 needs this pass's last level, R[d0+31][j]
+        // (lane 31's row of step j+30), copied once to shared memory so the
+        // pass's steps read it there instead of waiting on L2 (a desynchronised
+        // pair runs two passes per window)
+        {
+            const uint64_t* last = tab + (size_t)(d0 >> 5) * (96 * kFullLevels) + (kFullLevels - 1);
+            for (int x = q; x < n; x += kFullLevels) {
+                const uint64_t v = last[(size_t)(x + kFullLevels - 1) * kFullLevels];
+                pmt[64 + x] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+            }
+            __syncwarp();
+        }
     }
     return -1;
 }
@@ -1032,7 +1036,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(bt.pol));
 #endif
     uint64_t* ftab = reinterpret_cast<uint64_t*>(region);  // full tier reuses the region
-    __shared__ uint2 s_pm[kWarps][64];  // full tier: mismatch words per column
+    __shared__ uint2 s_pm[kWarps][128];  // full tier: mismatch words per column, carry row
     uint2* pmt = s_pm[threadIdx.x >> 5];
     const unsigned lt = lanemask_lt();
     bool exhausted = false;

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128) coop_bench_kernel(const thr::Planes* pp, 
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint64_t* tab = tabs + (size_t)gw * (kBandWordsPerWarp / 2);
-    __shared__ uint2 s_pm[4][64];
+    __shared__ uint2 s_pm[4][128];
     uint2* pmt = s_pm[threadIdx.x >> 5];
     unsigned long long tdc = 0, ttb = 0;
     for (int r = 0; r < reps; ++r) {
