@@ -808,34 +808,40 @@ __device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& 
                                         thr::TbOut& o, int lane) {
     using namespace thr;
     constexpr uint32_t kChars = '=' | 'X' << 8 | 'I' << 16 | 'D' << 24;
-    auto bit = [&](int e, int c, int x) -> uint32_t {
+    // row of level e at column c (full_index); lane q reads columns j-q-1 and
+    // j-q, so its rows are the uniform ones moved back q wavefront steps
+    auto row = [&](int e, int c) -> uint64_t {
         if (!GA_ASSERT(c >= 1 && c <= n && e >= 0 && e <= d_min &&
                            full_index(e, c) < kBandWordsPerWarp / 2,
                        3, e, c))
-            return 1u;
-        return (uint32_t)(tab[full_index(e, c)] >> x) & 1u;
+            return ~0ull;
+        return tab[full_index(e, c)];
     };
     int d = d_min, j = n, i = m - 1;
     o.consumed = o.tcons = o.wcost = 0;
-    o.reads = 0;
+    unsigned racc = 0;  // this lane's share of the entry reads, summed on return
+    auto done = [&](bool ok) {
+        o.reads = __reduce_add_sync(FULL, racc);
+        return ok;
+    };
     for (;;) {
-        if (i < 0 || o.consumed >= budget) return true;
+        if (i < 0 || o.consumed >= budget) return done(true);
         if (j == 0) {  // column 0: init zeros cover i+1 insertions at level d
-            if (i + 1 > d) return false;
+            if (i + 1 > d) return done(false);
             const int take = (i + 1 < budget - o.consumed) ? i + 1 : budget - o.consumed;
             for (int u = lane; u < take; u += 32) ops[nops + u] = 'I';
             nops += take;
             o.wcost += take;
             o.consumed += take;
-            return true;
+            return done(true);
         }
         const int jq = j - lane, iq = i - lane;
         int op = 4;  // this lane's state is past a limit: the run stops here
         unsigned rd = 0;
+        // symbol equality along the walk's diagonal, one mask for all lanes
+        const uint64_t eqv = diag_eq(pp, tp, i - j + 1);
         if (iq >= 0 && o.consumed + lane < budget && jq >= 1) {
-            const bool symeq = !bit64(tp.bn, jq - 1) && !bit64(pp.bn, iq) &&
-                               bit64(tp.b0, jq - 1) == bit64(pp.b0, iq) &&
-                               bit64(tp.b1, jq - 1) == bit64(pp.b1, iq);
+            const bool symeq = (eqv >> (jq - 1)) & 1ull;
             const int dm1 = d > 0 ? d - 1 : 0;
             uint32_t mb = 0, sb = 0, db, ib = 0;
             if (jq == 1) {  // column 0 = init(m, .): bit x inactive iff x >= level
@@ -843,13 +849,14 @@ __device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& 
                 sb = iq - 1 >= d - 1;
                 db = iq >= d - 1;
             } else {
+                const uint64_t rp = row(dm1, jq - 1);
                 if (iq >= 1) {
-                    mb = bit(d, jq - 1, iq - 1);
-                    sb = bit(dm1, jq - 1, iq - 1);
+                    mb = (uint32_t)(row(d, jq - 1) >> (iq - 1)) & 1u;
+                    sb = (uint32_t)(rp >> (iq - 1)) & 1u;
                 }
-                db = bit(dm1, jq - 1, iq);
+                db = (uint32_t)(rp >> iq) & 1u;
             }
-            if (iq >= 1) ib = bit(dm1, jq, iq - 1);
+            if (iq >= 1) ib = (uint32_t)(row(dm1, jq) >> (iq - 1)) & 1u;
             const bool dpos = d > 0;
             const bool mok = symeq && (iq == 0 || !mb);
             const bool sok = dpos && (iq == 0 || !sb);
@@ -864,15 +871,14 @@ __device__ __forceinline__ bool coop_tb(const uint64_t* tab, const thr::Planes& 
         const int f = nz ? __ffs(nz) - 1 : 32;
         const int opf = __shfl_sync(FULL, op, f & 31);
         const bool taken = f < 32 && opf <= OPC_D;  // lane f's step is taken too
-
-        o.reads += __reduce_add_sync(FULL, (lane < f || (taken && lane == f)) ? rd : 0u);
+        racc += (lane < f || (taken && lane == f)) ? rd : 0u;
         j -= f;
         i -= f;
         o.consumed += f;
         o.tcons += f;
         nops += f;
         if (f == 32 || opf == 4) continue;
-        if (opf > OPC_D) return false;
+        if (opf > OPC_D) return done(false);
         if (lane == 0) ops[nops] = (uint8_t)(kChars >> (8 * opf));
         ++nops;
         const int mj = opf != OPC_I, mi = opf != OPC_D;
