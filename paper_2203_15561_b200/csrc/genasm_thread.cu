@@ -449,10 +449,9 @@ __device__ __forceinline__ bool group_tb(const uint32_t* gtab, bool walk, const 
         const int jq = j - q, iq = i - q;
         int op = 4;  // this lane's state is past a limit (or the group is done): the run stops
         unsigned rd = 0;
+        const uint64_t eqv = diag_eq(pp, tp, i - j + 1);  // symbol equality along the diagonal
         if (!done && iq >= 0 && o.consumed + q < budget && jq >= 1) {
-            const bool symeq = !bit64(tp.bn, jq - 1) && !bit64(pp.bn, iq) &&
-                               bit64(tp.b0, jq - 1) == bit64(pp.b0, iq) &&
-                               bit64(tp.b1, jq - 1) == bit64(pp.b1, iq);
+            const bool symeq = (eqv >> (jq - 1)) & 1ull;
             const int dm1 = d > 0 ? d - 1 : 0;
             const int u = i - (o0 + j);  // band position of (iq, jq): the same along the diagonal
             uint32_t mb = 0, sb = 0, db, ib = 0;
