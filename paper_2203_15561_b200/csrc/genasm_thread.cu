@@ -32,7 +32,7 @@ namespace genasm {
 #ifdef GA_THREAD_STATS
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
-__device__ unsigned long long g_thread_stats[14];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB, [12] group window set-up
+__device__ unsigned long long g_thread_stats[17];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB, [12] group window set-up, [14]/[15]/[16] hand-over tail windows, their DC/TB cycles
 // per pair: first window started, finished (globaltimer ns), full-tier windows
 __device__ unsigned long long g_pair_t[3][262144];
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
@@ -919,6 +919,10 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
         d_min = coop_dc(pp, tp, w.m, w.n, P.k, kmax, ftab, pmt, lane);
 #ifdef GA_THREAD_STATS
         GA_STAT(10, clock64() - c0);
+        if (kmax > kFullLevels) {
+            GA_STAT(14, 1);
+            GA_STAT(15, clock64() - c0);
+        }
 #endif
         if (d_min < 0 && P.k > kmax) return true;
     }
@@ -936,6 +940,7 @@ __device__ __forceinline__ bool coop_window(const KernelParams& P, Lane& L, int 
                                 lane);
 #ifdef GA_THREAD_STATS
         GA_STAT(11, clock64() - c1);
+        if (kmax > kFullLevels) GA_STAT(16, clock64() - c1);
 #endif
         if (lane == owner) {
 #ifdef GA_THREAD_STATS
@@ -1364,9 +1369,9 @@ extern "C" void ga_debug_check(unsigned long long* out, int reset) {
 
 #ifdef GA_THREAD_STATS
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 14);
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 17);
     if (reset) {
-        unsigned long long z[14] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[17] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
         static unsigned long long pz[3][262144];
         for (int i = 0; i < 262144; ++i) pz[0][i] = ~0ull;

@@ -46,13 +46,13 @@ def main():
     dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
                            d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
     if hasattr(L, "ga_debug_thread_stats"):
-        z = np.zeros(14, np.uint64)
+        z = np.zeros(17, np.uint64)
         L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
     st = torch.cuda.Stream(dev)
     times = []
     for it in range(reps):
         if hasattr(L, "ga_debug_thread_stats") and it == reps - 1:
-            z = np.zeros(14, np.uint64)
+            z = np.zeros(17, np.uint64)
             L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -80,7 +80,7 @@ def main():
         np.savez_compressed(os.path.join("gpurun_out", f"pairtimes_r1_cfg{cfg_id}.npz"),
                             start=st_ms, fin=fin_ms, full=full)
     if hasattr(L, "ga_debug_thread_stats"):
-        st = np.zeros(14, np.uint64)
+        st = np.zeros(17, np.uint64)
         L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
         st = st.astype(np.float64)  # the last launch only
         print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
@@ -89,7 +89,8 @@ def main():
               f"warps finish own pairs over {(st[7] - st[6]) / 1e6:.2f} ms; lane 0 band DC cycles/step "
               f"{st[8] / max(st[0], 1):.0f} band TB cycles/step {st[9] / max(st[0], 1):.0f}; full-tier DC "
               f"cycles/window {st[10] / max(st[2], 1):.0f} TB {st[11] / max(st[2], 1):.0f}; group window "
-              f"set-up cycles/step {st[12] / max(st[0], 1):.0f}, traceback rounds/step {st[13] / max(st[0], 1):.1f}")
+              f"set-up cycles/step {st[12] / max(st[0], 1):.0f}, traceback rounds/step {st[13] / max(st[0], 1):.1f}; "
+              f"hand-over tail windows {st[14]:.0f}, DC {st[15] / max(st[14], 1):.0f} TB {st[16] / max(st[14], 1):.0f} cycles/window")
     import hashlib
     dig = hashlib.md5(res.cpu().numpy().tobytes() + dst.cpu().numpy().tobytes()).hexdigest()[:12]
     print(f"results+dists md5 {dig}")
