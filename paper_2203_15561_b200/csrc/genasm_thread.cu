@@ -32,9 +32,9 @@ namespace genasm {
 #ifdef GA_THREAD_STATS
 // dev counters: band steps, active lanes summed over band steps, full-tier
 // windows, -, clock cycles in band steps, in full-tier windows
-__device__ unsigned long long g_thread_stats[17];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB, [12] group window set-up, [14]/[15]/[16] hand-over tail windows, their DC/TB cycles
+__device__ unsigned long long g_thread_stats[18];  // [8]/[9] band DC/TB cycles, [10]/[11] full-tier DC/TB, [12] group window set-up, [14]/[15]/[16] hand-over tail windows, their DC/TB cycles
 // per pair: first window started, finished (globaltimer ns), full-tier windows
-__device__ unsigned long long g_pair_t[3][262144];
+__device__ unsigned long long g_pair_t[4][262144];  // + [3]: taken from the hand-over list
 #define GA_STAT(k, v) (lane == 0 ? (void)atomicAdd(&g_thread_stats[k], (unsigned long long)(v)) : (void)0)
 #else
 #define GA_STAT(k, v) ((void)0)
@@ -1236,9 +1236,22 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
         GA_ASSERT(pair < P.n_pairs, 6, pair, ticket);
         L.pair = -1;
         if (lane == 0) resume_pair(P, L, pair);
+#ifdef GA_THREAD_STATS
+        if (lane == 0 && pair < 262144) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            g_pair_t[3][pair] = tnow;
+        }
+#endif
         while (__shfl_sync(FULL, L.pair, 0) >= 0) {
             // lane 0 owns the pair; window_of() on lane 0's state drives all lanes
+#ifdef GA_THREAD_STATS
+            const long long tw = clock64();
+#endif
             if (coop_window(P, L, 0, lane, 1 << 30, ftab, pmt)) break;  // cannot: kmax covers k
+#ifdef GA_THREAD_STATS
+            GA_STAT(17, clock64() - tw);
+#endif
         }
     }
 }
@@ -1369,17 +1382,17 @@ extern "C" void ga_debug_check(unsigned long long* out, int reset) {
 
 #ifdef GA_THREAD_STATS
 extern "C" void ga_debug_thread_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 17);
+    cudaMemcpyFromSymbol(out, genasm::g_thread_stats, sizeof(unsigned long long) * 18);
     if (reset) {
-        unsigned long long z[17] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[18] = {0, 0, 0, 0, 0, 0, ~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(genasm::g_thread_stats, z, sizeof z);
-        static unsigned long long pz[3][262144];
+        static unsigned long long pz[4][262144];
         for (int i = 0; i < 262144; ++i) pz[0][i] = ~0ull;
         cudaMemcpyToSymbol(genasm::g_pair_t, pz, sizeof pz);
     }
 }
 extern "C" void ga_debug_pair_times(unsigned long long* out, int n) {
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < 4; ++k)
         cudaMemcpyFromSymbol(out + (size_t)k * n, genasm::g_pair_t, sizeof(unsigned long long) * n,
                              sizeof(unsigned long long) * 262144 * k);
 }

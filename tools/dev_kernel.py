@@ -46,13 +46,13 @@ def main():
     dout = _abi.GaBatchOut(res.data_ptr(), d[6].data_ptr(), ops.data_ptr(), host.n_ops,
                            d[7].data_ptr(), dst.data_ptr(), int(host.dists.shape[0]))
     if hasattr(L, "ga_debug_thread_stats"):
-        z = np.zeros(17, np.uint64)
+        z = np.zeros(18, np.uint64)
         L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
     st = torch.cuda.Stream(dev)
     times = []
     for it in range(reps):
         if hasattr(L, "ga_debug_thread_stats") and it == reps - 1:
-            z = np.zeros(17, np.uint64)
+            z = np.zeros(18, np.uint64)
             L.ga_debug_thread_stats(z.ctypes.data_as(C.c_void_p), 1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -64,23 +64,26 @@ def main():
         times.append(a.elapsed_time(b))
     r = res.cpu().numpy().view(_abi.RESULT_DTYPE)
     if hasattr(L, "ga_debug_pair_times") and n <= 262144:
-        pt = np.zeros(3 * n, np.uint64)
+        pt = np.zeros(4 * n, np.uint64)
         L.ga_debug_pair_times(pt.ctypes.data_as(C.c_void_p), n)
         t0 = pt[:n].min()
         st_ms = (pt[:n] - t0) / 1e6
         fin_ms = (pt[n:2 * n] - t0) / 1e6
-        full = pt[2 * n:].astype(np.int64)
+        full = pt[2 * n:3 * n].astype(np.int64)
+        ho = pt[3 * n:]
+        ho_ms = np.where(ho > 0, (ho.astype(np.float64) - t0) / 1e6, np.nan)
         q = [0, 1, 10, 50, 90, 99, 100]
         print("pair start ms pct " + " ".join(f"{p}:{np.percentile(st_ms, p):.1f}" for p in q))
         print("pair finish ms pct " + " ".join(f"{p}:{np.percentile(fin_ms, p):.1f}" for p in q))
         print("full-tier windows per pair pct " + " ".join(f"{p}:{np.percentile(full, p):.0f}" for p in q))
         slow = np.argsort(-fin_ms)[:8]
-        print("slowest pairs (id, finish ms, full-tier windows):",
-              [(int(i), round(float(fin_ms[i]), 1), int(full[i])) for i in slow])
+        print("slowest pairs (id, finish ms, full-tier windows, taken from the hand-over list ms):",
+              [(int(i), round(float(fin_ms[i]), 1), int(full[i]), round(float(ho_ms[i]), 1)) for i in slow])
+        print("handed-over pairs", int(np.isfinite(ho_ms).sum()))
         np.savez_compressed(os.path.join("gpurun_out", f"pairtimes_r1_cfg{cfg_id}.npz"),
-                            start=st_ms, fin=fin_ms, full=full)
+                            start=st_ms, fin=fin_ms, full=full, handover=ho_ms)
     if hasattr(L, "ga_debug_thread_stats"):
-        st = np.zeros(17, np.uint64)
+        st = np.zeros(18, np.uint64)
         L.ga_debug_thread_stats(st.ctypes.data_as(C.c_void_p), 1)
         st = st.astype(np.float64)  # the last launch only
         print(f"band steps/launch {st[0]:.0f} active lanes/step {st[1] / max(st[0], 1):.2f} "
@@ -90,7 +93,8 @@ def main():
               f"{st[8] / max(st[0], 1):.0f} band TB cycles/step {st[9] / max(st[0], 1):.0f}; full-tier DC "
               f"cycles/window {st[10] / max(st[2], 1):.0f} TB {st[11] / max(st[2], 1):.0f}; group window "
               f"set-up cycles/step {st[12] / max(st[0], 1):.0f}, traceback rounds/step {st[13] / max(st[0], 1):.1f}; "
-              f"hand-over tail windows {st[14]:.0f}, DC {st[15] / max(st[14], 1):.0f} TB {st[16] / max(st[14], 1):.0f} cycles/window")
+              f"hand-over tail windows {st[14]:.0f}, DC {st[15] / max(st[14], 1):.0f} TB {st[16] / max(st[14], 1):.0f} "
+              f"whole window {st[17] / max(st[14], 1):.0f} cycles")
     import hashlib
     dig = hashlib.md5(res.cpu().numpy().tobytes() + dst.cpu().numpy().tobytes()).hexdigest()[:12]
     print(f"results+dists md5 {dig}")
