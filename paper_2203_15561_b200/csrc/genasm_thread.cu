@@ -785,7 +785,10 @@ __device__ __forceinline__ void hand_over(const KernelParams& P, Lane& L, const 
 
 __device__ __forceinline__ void resume_pair(const KernelParams& P, Lane& L, int pair) {
     fresh_pair(P, L, pair);
-    const PairResult* r = reinterpret_cast<const PairResult*>(P.results) + pair;
+    // the parked state was written by another SM: read it from L2 (volatile),
+    // never from a line this SM's L1 may hold from an earlier resume of the
+    // record next to it
+    const volatile PairResult* r = reinterpret_cast<const volatile PairResult*>(P.results) + pair;
     L.widx = r->fail_window;
     L.cost = r->cost;
     L.t = r->text_consumed;
