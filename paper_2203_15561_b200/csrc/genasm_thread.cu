@@ -74,7 +74,12 @@ namespace {
 constexpr int kTBlock = GA_TBLOCK;  // threads per block
 constexpr int kWarps = kTBlock / 32;
 constexpr int kFullLevels = 32;  // full tier: one level per lane
-constexpr int kStreak = 4;       // consecutive full-tier windows before a hand-over
+// consecutive full-tier windows before a hand-over: 8 for the lane-per-pair
+// launches (config 3 37.1 -> 36.4 ms against 4: a pair over a long indel
+// stays in its lane instead of running all its remaining windows on a whole
+// warp; 2: 101 ms), 4 for the lane groups (config 5 10.6 ms against 11.1)
+constexpr int kStreak = 8;
+constexpr int kStreakGroups = 4;
 constexpr int kBandWordsPerWarp = 64 * 2 * 32 * 4;  // W <= 64 columns x 8 paired words x 32 lanes
 
 // full-tier table: [pass][wavefront step][level within the pass], 24 KB per
@@ -1127,7 +1132,7 @@ genasm_thread_kernel(const KernelParams P, uint32_t* band_base, const HandList H
             // divergent sequences) is handed over: the warps that run out of
             // pairs finish it, so it does not hold its warp back
             L.streak = r == WIN_HARD ? L.streak + 1 : 0;
-            if (L.streak >= kStreak) {
+            if (L.streak >= (kGroup ? kStreakGroups : kStreak)) {
                 hand_over(P, L, H);
                 r = WIN_NEXT;
             }
