@@ -1309,8 +1309,20 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     const int sm_share = !group && P.n_pairs < resident && !P.overlapped
                              ? (int)((P.n_pairs + num_sms - 1) / num_sms) : 0;
     const int64_t lanes = P.n_pairs < resident ? P.n_pairs : resident;
-    int grid = sm_share ? num_sms * per_sm : (int)((lanes + kTBlock - 1) / kTBlock > 0
-                                                   ? (lanes + kTBlock - 1) / kTBlock : 1);
+    // The equal-share launch keeps only the blocks a SM's share needs, and at
+    // least two: the warps beyond the share (they serve the hand-overs) take
+    // issue slots from the working ones.  Config 4 (135 pairs per SM): 8 warps
+    // per SM 76.0 ms, 12 83.5, 16 85.6; config 3's 17,367-pair shard 9.96 /
+    // 10.37 / 9.90 ms.  GA_SHARE_BLOCKS overrides the count.
+    int per_sm_share = per_sm;
+    if (sm_share) {
+        const char* sb = getenv("GA_SHARE_BLOCKS");
+        const int need = (sm_share + kTBlock - 1) / kTBlock;
+        per_sm_share = sb && atoi(sb) > 0 ? atoi(sb) : (need > 2 ? need : 2);
+        if (per_sm_share > per_sm) per_sm_share = per_sm;
+    }
+    int grid = sm_share ? num_sms * per_sm_share : (int)((lanes + kTBlock - 1) / kTBlock > 0
+                                                         ? (lanes + kTBlock - 1) / kTBlock : 1);
     if (group) {
         // a block per SM more than the pairs need, where it fits: its warps
         // find no pair and stay to take hand-overs at once (the tail below)
@@ -1370,7 +1382,7 @@ cudaError_t launch_genasm_thread(const KernelParams& base, int num_sms, cudaStre
     shape->block = kTBlock;
     shape->smem_bytes = group ? (int)gsmem : 0;
     shape->group = group ? kGroupLanes : 1;
-    shape->blocks_per_sm = group ? per_sm_g : per_sm;
+    shape->blocks_per_sm = group ? per_sm_g : (sm_share ? per_sm_share : per_sm);
     shape->overflow_words_per_group = 0;
     shape->launches = 2;
     return cudaGetLastError();
